@@ -1,0 +1,114 @@
+/* pipesgd.h — C ABI of the B200-native Pipe-SGD communication hot path.
+ *
+ * libpipesgd.so (paper_1811_03619_b200/libpipesgd.so) exports exactly the
+ * functions below: plain pointers, sizes and CUDA stream handles, no torch
+ * types. Device pointers are CUDA device addresses on the communicator's
+ * device (or the current device for the stateless codec/update calls);
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Each entry replaces a function of the reference package `gradpipe`
+ * (/root/reference/pkg/src/gradpipe):
+ *   gp_allreduce            collective.py:143-163 ring_allreduce
+ *                           collective.py:166-212 pipelined_allreduce (same bits)
+ *   gp_allreduce_emulated   the same ring with all p ranks on one device
+ *                           (collective.py:77-139 driven like tests/helpers.py:10-29)
+ *   gp_comm_create/connect  transport.py:150-177 InProcTransport(world).endpoint(r)
+ *                           transport.py:192-305 TcpEndpoint mesh set-up
+ *   gp_get_stats/reset      transport.py:52-61, :85-91, :105-107 TrafficStats
+ *   gp_comm_poll_error      collective.py:52-64, :157-161 CollectiveError,
+ *                           compression.py:108-109 CodecError (non-finite)
+ *   gp_encode / gp_decode   compression.py:103-136 compress, :141-151 decompress
+ *   gp_roundtrip            engine.py:333 + :355/:400 decompress(compress(grad))
+ *   gp_consume_update       engine.py:420-426 decompress -> engine.py:123-129
+ *                           aggregate_mean -> models.py:198-204 sgd_update
+ *
+ * Return value: GP_OK (0) or a GP_ERR_* code; gp_last_error_string() gives
+ * the calling thread's last message. Failures detected on the device
+ * (non-finite values, ring timeouts, header mismatches) are latched in a
+ * device error word and reported by gp_comm_poll_error / gp_codec_status.
+ */
+#ifndef PIPESGD_H_
+#define PIPESGD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gp_comm gp_comm;
+
+enum { GP_CODEC_NONE = 0, GP_CODEC_TRUNC16 = 1, GP_CODEC_QUANT8 = 2 };
+
+enum {
+  GP_OK = 0,
+  GP_ERR_ARG = 1,         /* bad argument (codec, size, alignment, aliasing) */
+  GP_ERR_CUDA = 2,        /* CUDA runtime failure */
+  GP_ERR_STATE = 3,       /* communicator not connected / wrong mode */
+  GP_ERR_UNSUPPORTED = 4  /* e.g. no peer access between two devices */
+};
+
+/* device failure kinds (gp_error.kind, gp_codec_status.nonfinite) */
+enum { GP_FAIL_NONE = 0, GP_FAIL_NONFINITE = 1, GP_FAIL_TIMEOUT = 2, GP_FAIL_HEADER = 3 };
+/* gp_error.phase */
+enum { GP_PHASE_REDUCE_SCATTER = 0, GP_PHASE_ALLGATHER = 1, GP_PHASE_BARRIER = 2 };
+
+typedef struct {
+  int32_t kind;   /* GP_FAIL_* */
+  int32_t phase;  /* GP_PHASE_* */
+  int32_t step;   /* reference ring step within the phase */
+  int32_t block;  /* block index (partition_blocks order), -1 if n/a */
+  int32_t rank;   /* rank that observed the failure */
+  int32_t detail; /* TIMEOUT: 1 = a peer aborted first; HEADER: advertised n_elems */
+} gp_error;
+
+typedef struct {
+  uint64_t messages;      /* data messages sent: 2(p-1) per allreduce */
+  uint64_t payload_bytes; /* codec payload bytes, 9-byte block header excluded */
+  uint64_t frame_bytes;   /* payload + 9-byte block header + 11-byte frame header */
+} gp_stats;
+
+/* Device-resident status of a stateless codec call (16 bytes, device memory). */
+typedef struct {
+  uint32_t absmax_bits; /* bits of max|x| (quant8) */
+  int32_t nonfinite;    /* != 0: a NaN/Inf was seen -> CodecError */
+  float scale;          /* quant8 block scale written by gp_encode */
+  uint32_t reserved;
+} gp_codec_status;
+
+/* ---- communicator (one per rank) ------------------------------------- */
+int gp_comm_create(int rank, int world, int device, uint64_t max_elems, gp_comm** out);
+int gp_comm_create_emulated(int world, int device, uint64_t max_elems, gp_comm** out);
+int gp_comm_ipc_handle(gp_comm* comm, void* handle_out /* 64 bytes */);
+int gp_comm_connect_ipc(gp_comm* comm, const void* handles /* world x 64 bytes, rank order */);
+int gp_comm_connect_local(gp_comm* const* comms, int world);
+int gp_comm_set_tuning(gp_comm* comm, int ctas_per_rank, double timeout_s);
+int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, emulated] */);
+int gp_comm_destroy(gp_comm* comm);
+
+int gp_allreduce(gp_comm* comm, const float* in, float* out, uint64_t n, int codec,
+                 uint32_t iteration, void* stream);
+int gp_allreduce_emulated(gp_comm* comm, const float* const* ins, float* const* outs, uint64_t n,
+                          int codec, uint32_t iteration, void* stream);
+int gp_comm_poll_error(gp_comm* comm, gp_error* out); /* call after the stream completed; clears */
+int gp_get_stats(gp_comm* comm, int rank, gp_stats* out);
+int gp_reset_stats(gp_comm* comm);
+
+/* ---- stateless codec / update kernels (current device) ---------------- */
+int gp_encode(int codec, const float* in, uint64_t n, void* payload, gp_codec_status* status,
+              void* stream);
+int gp_decode(int codec, const void* payload, const float* scale /* device, quant8 */, uint64_t n,
+              float* out, void* stream);
+int gp_roundtrip(int codec, const float* in, float* out, uint64_t n, gp_codec_status* status,
+                 void* stream);
+int gp_consume_update(float* params, int codec, const void* slot, const float* slot_scale,
+                      uint64_t n, float lr, int world, void* stream);
+
+const char* gp_last_error_string(void);
+int gp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPESGD_H_ */

@@ -1,0 +1,379 @@
+// Communicator: inbox allocation, peer mapping (in-process peer access or
+// CUDA IPC between torchrun processes), ring launch, traffic accounting and
+// device error reporting. Replaces the reference transport for this path
+// (transport.py:44-177) — send/recv disappear into the fused kernel; the
+// endpoint bookkeeping (rank, world, timeout, stats) stays.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/pipesgd.h"
+#include "ring.cuh"
+
+using namespace gp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const std::string& what) {
+  return fail(GP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+Layout make_layout(int p, uint64_t max_elems) {
+  Layout L{};
+  const uint64_t maxblk = (max_elems + p - 1) / p;
+  L.nslot = (uint32_t)(2 * p - 1);
+  L.slot_bytes = round_up((maxblk + 16) * 4, 256);
+  L.max_chunks = (uint32_t)((maxblk + 8 + kMinChunk - 1) / kMinChunk + 1);
+  L.off_ctl = 0;
+  L.off_err = 4096;
+  L.off_hdr = 4096 + 256;
+  L.off_flags = round_up(L.off_hdr + (uint64_t)L.nslot * sizeof(SlotHdr), 256);
+  L.off_payload = round_up(L.off_flags + (uint64_t)L.nslot * L.max_chunks * 8, 4096);
+  L.total_bytes = L.off_payload + (uint64_t)L.nslot * L.slot_bytes;
+  return L;
+}
+
+}  // namespace
+
+void gp_set_error_string(const std::string& m) { g_err = m; }
+
+struct gp_comm {
+  int rank = 0, world = 1, device = 0;
+  uint64_t max_elems = 0;
+  Layout L{};
+  int nlocal = 1;                       // p when emulated
+  uint8_t* inbox[kMaxRanks] = {};       // local allocations (1, or p when emulated)
+  uint8_t* peer[kMaxRanks] = {};        // every rank's inbox as mapped on this device
+  bool ipc_opened[kMaxRanks] = {};
+  bool connected = false;
+  uint32_t seq = 0;
+  unsigned long long bar_total = 0;
+  int G = 0;
+  double timeout_s = 30.0;
+  gp_stats stats[kMaxRanks] = {};
+};
+
+namespace {
+
+int alloc_inbox(gp_comm* c, int i) {
+  cudaError_t e = cudaMalloc(&c->inbox[i], c->L.total_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(inbox)");
+  // Flags, headers, ctl and error word must start at zero; payload need not.
+  e = cudaMemset(c->inbox[i], 0, c->L.off_payload);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(inbox)");
+  return GP_OK;
+}
+
+int default_ctas(int device) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return std::max(1, std::min(64, sms / 2));
+}
+
+void count_message(gp_stats& s, int codec, uint64_t len) {
+  const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
+  s.messages += 1;
+  s.payload_bytes += len * w;
+  s.frame_bytes += 11 + 9 + len * w;  // transport.py:37 frame + compression.py:33 header
+}
+
+// Reference accounting: rank r sends blocks (r-s)%p in reduce-scatter and
+// (r+1-s)%p in allgather, s = 0..p-2 (collective.py:97-99, :125-127).
+void account(gp_stats& s, int rank, int p, uint64_t n, int codec) {
+  for (int st = 0; st < p - 1; ++st) {
+    uint64_t off, len;
+    block_range(n, p, ((rank - st) % p + p) % p, off, len);
+    count_message(s, codec, len);
+  }
+  for (int st = 0; st < p - 1; ++st) {
+    uint64_t off, len;
+    block_range(n, p, ((rank + 1 - st) % p + p) % p, off, len);
+    count_message(s, codec, len);
+  }
+}
+
+uint32_t pick_chunk(uint64_t n, int p, int G) {
+  const uint64_t maxblk = (n + p - 1) / p + 8;
+  uint64_t ch = round_up((maxblk + G - 1) / G, kMinChunk);
+  ch = std::max<uint64_t>(kMinChunk, std::min<uint64_t>(kMaxChunk, ch));
+  return (uint32_t)ch;
+}
+
+int check_common(gp_comm* c, uint64_t n, int codec) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  if (codec < 0 || codec > 2) return fail(GP_ERR_ARG, "unknown codec " + std::to_string(codec));
+  if (n > c->max_elems)
+    return fail(GP_ERR_ARG, "vector of " + std::to_string(n) + " elems exceeds communicator capacity " +
+                                std::to_string(c->max_elems));
+  if (n >= (1ull << 32) * (uint64_t)c->world) return fail(GP_ERR_ARG, "block exceeds 2^32 elements");
+  return GP_OK;
+}
+
+bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* gp_last_error_string(void) { return g_err.c_str(); }
+int gp_version(void) { return 1; }
+
+int gp_comm_create(int rank, int world, int device, uint64_t max_elems, gp_comm** out) {
+  if (!out) return fail(GP_ERR_ARG, "null out");
+  if (world < 1 || world > kMaxRanks) return fail(GP_ERR_ARG, "world size must be in [1, 8]");
+  if (rank < 0 || rank >= world)
+    return fail(GP_ERR_ARG, "rank " + std::to_string(rank) + " outside [0, " + std::to_string(world) + ")");
+  DeviceGuard g(device);
+  gp_comm* c = new gp_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->max_elems = std::max<uint64_t>(max_elems, 1);
+  c->L = make_layout(world, c->max_elems);
+  c->G = default_ctas(device);
+  int rc = alloc_inbox(c, 0);
+  if (rc) { delete c; return rc; }
+  c->peer[rank] = c->inbox[0];
+  if (world == 1) c->connected = true;
+  *out = c;
+  return GP_OK;
+}
+
+int gp_comm_create_emulated(int world, int device, uint64_t max_elems, gp_comm** out) {
+  if (!out) return fail(GP_ERR_ARG, "null out");
+  if (world < 1 || world > kMaxRanks) return fail(GP_ERR_ARG, "world size must be in [1, 8]");
+  DeviceGuard g(device);
+  gp_comm* c = new gp_comm();
+  c->world = world;
+  c->device = device;
+  c->nlocal = world;
+  c->max_elems = std::max<uint64_t>(max_elems, 1);
+  c->L = make_layout(world, c->max_elems);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  // all p x G CTAs must be co-resident (2 x 512-thread CTAs per SM)
+  c->G = std::max(1, std::min(16, (2 * sms) / world));
+  for (int i = 0; i < world; ++i) {
+    int rc = alloc_inbox(c, i);
+    if (rc) { for (int k = 0; k < i; ++k) cudaFree(c->inbox[k]); delete c; return rc; }
+    c->peer[i] = c->inbox[i];
+  }
+  c->connected = true;
+  *out = c;
+  return GP_OK;
+}
+
+int gp_comm_ipc_handle(gp_comm* c, void* handle_out) {
+  if (!c || !handle_out) return fail(GP_ERR_ARG, "null argument");
+  if (c->nlocal != 1) return fail(GP_ERR_STATE, "emulated communicator has no IPC handle");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, c->inbox[0]);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle_out, &h, 64);
+  return GP_OK;
+}
+
+int gp_comm_connect_ipc(gp_comm* c, const void* handles) {
+  if (!c || !handles) return fail(GP_ERR_ARG, "null argument");
+  if (c->nlocal != 1) return fail(GP_ERR_STATE, "emulated communicator");
+  DeviceGuard g(c->device);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * q, 64);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle(rank " + std::to_string(q) + ")");
+    c->peer[q] = static_cast<uint8_t*>(ptr);
+    c->ipc_opened[q] = true;
+  }
+  c->connected = true;
+  return GP_OK;
+}
+
+int gp_comm_connect_local(gp_comm* const* comms, int world) {
+  if (!comms || world < 1 || world > kMaxRanks) return fail(GP_ERR_ARG, "bad communicator list");
+  for (int i = 0; i < world; ++i) {
+    if (!comms[i] || comms[i]->world != world || comms[i]->rank != i || comms[i]->nlocal != 1)
+      return fail(GP_ERR_ARG, "communicator list must hold ranks 0..world-1 of one world");
+    for (int k = 0; k < i; ++k)
+      if (comms[k]->device == comms[i]->device)
+        return fail(GP_ERR_UNSUPPORTED,
+                    "ranks " + std::to_string(k) + " and " + std::to_string(i) +
+                        " share device " + std::to_string(comms[i]->device) +
+                        "; use the emulated communicator for more ranks than GPUs");
+  }
+  for (int i = 0; i < world; ++i) {
+    DeviceGuard g(comms[i]->device);
+    for (int k = 0; k < world; ++k) {
+      if (k == i) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, comms[i]->device, comms[k]->device);
+      if (!can)
+        return fail(GP_ERR_UNSUPPORTED, "device " + std::to_string(comms[i]->device) +
+                                            " cannot access device " + std::to_string(comms[k]->device));
+      cudaError_t e = cudaDeviceEnablePeerAccess(comms[k]->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+      comms[i]->peer[k] = comms[k]->inbox[0];
+    }
+    comms[i]->connected = true;
+  }
+  return GP_OK;
+}
+
+int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  if (ctas > 0) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int cap = c->nlocal == 1 ? sms : std::max(1, (2 * sms) / c->nlocal);
+    c->G = std::min(ctas, cap);
+  }
+  if (timeout_s > 0) c->timeout_s = timeout_s;
+  return GP_OK;
+}
+
+int gp_comm_info(gp_comm* c, int64_t* o) {
+  if (!c || !o) return fail(GP_ERR_ARG, "null argument");
+  o[0] = c->rank; o[1] = c->world; o[2] = c->device; o[3] = (int64_t)c->max_elems;
+  o[4] = c->G; o[5] = (int64_t)c->L.total_bytes; o[6] = c->seq; o[7] = c->nlocal > 1;
+  return GP_OK;
+}
+
+int gp_comm_destroy(gp_comm* c) {
+  if (!c) return GP_OK;
+  DeviceGuard g(c->device);
+  for (int q = 0; q < kMaxRanks; ++q)
+    if (c->ipc_opened[q]) cudaIpcCloseMemHandle(c->peer[q]);
+  for (int i = 0; i < c->nlocal; ++i)
+    if (c->inbox[i]) cudaFree(c->inbox[i]);
+  delete c;
+  return GP_OK;
+}
+
+static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int codec,
+                  uint32_t iteration, cudaStream_t st) {
+  const int p = c->world;
+  if (p == 1) {
+    if (n) {
+      cudaError_t e = cudaMemcpyAsync(outs[0], ins[0], n * 4, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
+    }
+    return GP_OK;
+  }
+  RingParams P{};
+  P.L = c->L;
+  P.n = n;
+  P.p = p;
+  P.codec = codec;
+  P.G = c->G;
+  P.seq = ++c->seq;
+  P.iteration = iteration;
+  P.chunk = pick_chunk(n, p, c->G);
+  P.bar_base = c->bar_total;
+  P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
+  for (int i = 0; i < c->nlocal; ++i) {
+    RankCtx& R = P.rk[i];
+    R.x = ins[i];
+    R.out = outs[i];
+    R.rank = c->nlocal == 1 ? c->rank : i;
+    R.inbox = c->inbox[i];
+    for (int q = 0; q < p; ++q) R.peer[q] = c->peer[q];
+  }
+  cudaError_t e;
+  launch_ring(P, c->nlocal, st, &e);
+  if (e != cudaSuccess) return cuda_fail(e, "ring kernel launch");
+  if (codec == GP_CODEC_QUANT8) c->bar_total += (unsigned long long)p * c->G;
+  for (int i = 0; i < c->nlocal; ++i) account(c->stats[i], P.rk[i].rank, p, n, codec);
+  return GP_OK;
+}
+
+int gp_allreduce(gp_comm* c, const float* in, float* out, uint64_t n, int codec, uint32_t iteration,
+                 void* stream) {
+  int rc = check_common(c, n, codec);
+  if (rc) return rc;
+  if (c->nlocal != 1) return fail(GP_ERR_STATE, "use gp_allreduce_emulated on an emulated communicator");
+  if (!c->connected) return fail(GP_ERR_STATE, "communicator is not connected to its peers");
+  if (n && (!in || !out)) return fail(GP_ERR_ARG, "null buffer");
+  if (n && (misaligned(in) || misaligned(out))) return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
+  if (n && in < out + n && out < in + n) return fail(GP_ERR_ARG, "input and output overlap");
+  DeviceGuard g(c->device);
+  return launch(c, &in, &out, n, codec, iteration, static_cast<cudaStream_t>(stream));
+}
+
+int gp_allreduce_emulated(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int codec,
+                          uint32_t iteration, void* stream) {
+  int rc = check_common(c, n, codec);
+  if (rc) return rc;
+  if (c->nlocal == 1 && c->world > 1) return fail(GP_ERR_STATE, "not an emulated communicator");
+  for (int i = 0; i < c->nlocal; ++i) {
+    if (n && (!ins[i] || !outs[i])) return fail(GP_ERR_ARG, "null buffer");
+    if (n && (misaligned(ins[i]) || misaligned(outs[i]))) return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
+  }
+  DeviceGuard g(c->device);
+  return launch(c, ins, outs, n, codec, iteration, static_cast<cudaStream_t>(stream));
+}
+
+int gp_comm_poll_error(gp_comm* c, gp_error* out) {
+  if (!c || !out) return fail(GP_ERR_ARG, "null argument");
+  DeviceGuard g(c->device);
+  std::memset(out, 0, sizeof(*out));
+  for (int i = 0; i < c->nlocal; ++i) {
+    ErrWord w;
+    cudaError_t e = cudaMemcpy(&w, c->inbox[i] + c->L.off_err, sizeof(w), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(error word)");
+    if (w.kind != 0) {
+      if (out->kind == 0) {
+        out->kind = w.kind; out->phase = w.phase; out->step = w.step;
+        out->block = w.block; out->rank = w.rank; out->detail = w.detail;
+      }
+      e = cudaMemset(c->inbox[i] + c->L.off_err, 0, sizeof(ErrWord));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(error word)");
+    }
+  }
+  return GP_OK;
+}
+
+int gp_get_stats(gp_comm* c, int rank, gp_stats* out) {
+  if (!c || !out) return fail(GP_ERR_ARG, "null argument");
+  const int i = c->nlocal == 1 ? 0 : rank;
+  if (i < 0 || i >= c->nlocal) return fail(GP_ERR_ARG, "rank outside communicator");
+  *out = c->stats[i];
+  return GP_OK;
+}
+
+int gp_reset_stats(gp_comm* c) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  for (auto& s : c->stats) s = gp_stats{};
+  return GP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// Fused compressed ring AllReduce — shared declarations between the kernel
+// (ring.cu) and the communicator (comm.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace gp {
+
+constexpr int kRingThreads = 512;
+constexpr uint32_t kMinChunk = 1024;   // elements; flags are sized for this
+constexpr uint32_t kMaxChunk = 16384;  // elements per chunk (64 KiB of fp32)
+
+// Per-rank inbox layout (identical on every rank of a communicator). Peers
+// write payload, headers and flags here over NVLink; ctl/err are private.
+struct Layout {
+  uint64_t off_ctl, off_err, off_hdr, off_flags, off_payload;
+  uint64_t slot_bytes;   // payload bytes per slot
+  uint64_t total_bytes;
+  uint32_t max_chunks;   // flags per slot
+  uint32_t nslot;        // 2p-1: p-1 reduce-scatter slots + p allgather slots
+};
+
+struct Ctl {                   // rank-private control block
+  unsigned long long bar;      // monotonic barrier arrival counter
+  unsigned long long abort;    // == seq when this call aborted
+  unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier
+};
+
+struct SlotHdr {               // written by the sender before each chunk flag
+  uint32_t seq, iteration, block, n_elems;
+  float scale;
+  uint32_t pad[11];
+};
+
+struct RankCtx {
+  const float* x;              // this rank's input vector (n)
+  float* out;                  // this rank's output vector (n)
+  uint8_t* inbox;              // this rank's inbox (local HBM)
+  uint8_t* peer[kMaxRanks];    // every rank's inbox as seen from this GPU
+  int rank;
+};
+
+struct RingParams {
+  RankCtx rk[kMaxRanks];       // one entry per rank in this launch (1, or p when emulated)
+  Layout L;
+  uint64_t n;
+  unsigned long long bar_base; // Ctl::bar value at entry
+  uint64_t timeout_ns;
+  uint32_t seq, iteration;
+  uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
+  int p, codec, G;             // world size, codec tag, CTAs per rank
+};
+
+__host__ __device__ inline int rs_slot(int s) { return s; }
+__host__ __device__ inline int ag_slot(int p, int b) { return p - 1 + b; }
+
+// partition_blocks (collective.py:35-49)
+__host__ __device__ inline void block_range(uint64_t n, int p, int b, uint64_t& start, uint64_t& len) {
+  const uint64_t base = n / p, extra = n % p;
+  start = (uint64_t)b * base + ((uint64_t)b < extra ? (uint64_t)b : extra);
+  len = base + ((uint64_t)b < extra ? 1 : 0);
+}
+
+void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError_t* err);
+
+}  // namespace gp

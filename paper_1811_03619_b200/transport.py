@@ -1,0 +1,327 @@
+"""GPU transports: NVLink/NVSwitch peer memory instead of queues and sockets.
+
+Drop-in for the endpoint side of /root/reference/pkg/src/gradpipe/transport.py.
+The reference moves serialized blocks through per-pair FIFO channels
+(`InProcTransport`, :150-177; `TcpEndpoint`, :192-305) and counts outgoing
+traffic per endpoint (`TrafficStats`, :52-61, :85-91). Here the fused ring
+kernel writes straight into the successor's inbox over NVLink, so `send` /
+`recv` do not exist; what remains is the endpoint bookkeeping the callers
+use — `rank`, `world_size`, `timeout_s`, `latency_s`, `byte_time_s`,
+`stats`, `reset_stats()`, `close()` — with identical accounting (data
+messages, codec payload bytes without the 9-byte header, frame bytes with
+the 11-byte frame header).
+
+Three ways to build endpoints:
+  * GpuTransport(world_size)            one process, rank r on cuda:r, peer
+                                        access between all pairs (mirrors
+                                        InProcTransport: p threads, one per rank)
+  * EmulatedTransport(world_size)       p ranks on ONE GPU: the ranks' calls
+                                        rendezvous and one cooperative launch
+                                        runs the whole ring (parity at p > #GPUs)
+  * ProcessGroupTransport.endpoint()    one process per GPU under torchrun;
+                                        inboxes shared through CUDA IPC handles
+                                        exchanged over torch.distributed
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import CodecError, CollectiveError, ConfigError
+
+DEFAULT_TIMEOUT_S = 30.0
+DEFAULT_MAX_ELEMS = 1 << 26  # 256 MiB of fp32 per allreduce; inbox ~ 2x that per rank
+
+
+@dataclass
+class TrafficStats:
+    """Outgoing-traffic counters for one endpoint (data messages only)."""
+
+    messages: int = 0
+    payload_bytes: int = 0
+    frame_bytes: int = 0
+
+    def snapshot(self) -> "TrafficStats":
+        return TrafficStats(self.messages, self.payload_bytes, self.frame_bytes)
+
+
+_PHASE = {0: "reduce-scatter", 1: "allgather", 2: "reduce-scatter barrier"}
+
+
+def _comm_create(rank: int, world: int, device: int, max_elems: int) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _lib.call("gp_comm_create", rank, world, device, max_elems, ctypes.byref(h))
+    return h
+
+
+class GpuEndpoint:
+    """One rank's view of the GPU ring (the reference's Endpoint surface)."""
+
+    def __init__(self, rank: int, world_size: int, device: torch.device, comm, timeout_s: float,
+                 vrank_of=None, transport=None):
+        if not 0 <= rank < world_size:
+            raise ConfigError(f"rank {rank} outside [0, {world_size})")
+        self.rank = rank
+        self.world_size = world_size
+        self.device = device
+        self.timeout_s = timeout_s
+        self.latency_s = 0.0       # no injected delay: the link is real
+        self.byte_time_s = 0.0
+        self._comm = comm
+        self._transport = transport
+        self._stats_base = TrafficStats()
+        self._poisoned: str | None = None
+        self.closed = False
+
+    # -- reference Endpoint surface -------------------------------------
+    @property
+    def stats(self) -> TrafficStats:
+        raw = self._raw_stats()
+        b = self._stats_base
+        return TrafficStats(raw.messages - b.messages, raw.payload_bytes - b.payload_bytes,
+                            raw.frame_bytes - b.frame_bytes)
+
+    def reset_stats(self) -> None:
+        self._stats_base = self._raw_stats()
+
+    def close(self) -> None:
+        self.closed = True
+
+    def send(self, *a, **k):  # pragma: no cover - documented absence
+        raise CollectiveError("GPU endpoints have no point-to-point send; the ring kernel moves the data")
+
+    recv = send
+
+    # -- internals --------------------------------------------------------
+    def _raw_stats(self) -> TrafficStats:
+        s = _lib.GpStats()
+        _lib.call("gp_get_stats", self._comm, self.rank, ctypes.byref(s))
+        return TrafficStats(int(s.messages), int(s.payload_bytes), int(s.frame_bytes))
+
+    def _launch(self, x: torch.Tensor, out: torch.Tensor, codec: int, iteration: int, stream: int) -> None:
+        if self._poisoned:
+            raise CollectiveError(f"endpoint {self.rank} is unusable after an earlier failure: {self._poisoned}")
+        _lib.call("gp_allreduce", self._comm, x.data_ptr(), out.data_ptr(), x.numel(), int(codec),
+                  int(iteration) & 0xFFFFFFFF, stream)
+
+    def _check_errors(self, n: int) -> None:
+        """After the launching stream completed: raise what the device latched."""
+        e = _lib.GpError()
+        _lib.call("gp_comm_poll_error", self._comm, ctypes.byref(e))
+        if e.kind:
+            raise self._poison(raise_for(e, self.world_size, n, self.timeout_s))
+
+    def _poison(self, err: Exception) -> Exception:
+        if isinstance(err, CollectiveError):
+            self._poisoned = str(err)
+        return err
+
+
+def raise_for(e, p: int, n: int, timeout_s: float) -> Exception:
+    """Map a device error word to the reference's exception and message shape
+    (collective.py:52-64, :106, :157-161; compression.py:108-109)."""
+    if e.kind == _lib.GP_FAIL_NONFINITE:
+        return CodecError("refusing to compress non-finite values")
+    phase = _PHASE.get(e.phase, "ring")
+    pred = (e.rank - 1) % p
+    if e.kind == _lib.GP_FAIL_TIMEOUT:
+        why = "aborted after a peer failed" if e.detail == 1 else f"timed out after {timeout_s:g}s"
+        return CollectiveError(f"{phase} step {e.step} (rank {e.rank} <- {pred}): {why}"
+                               + (f" waiting for block {e.block}" if e.block >= 0 else ""))
+    if e.kind == _lib.GP_FAIL_HEADER:
+        from .collective import partition_blocks
+        want = partition_blocks(n, p)[e.block][1] if 0 <= e.block < p else -1
+        return CollectiveError(f"{phase} step {e.step}: block {e.block} has {e.detail} elems, expected "
+                               f"{want} or a different iteration tag (unequal vector lengths across ranks?)")
+    return CollectiveError(f"{phase} step {e.step}: device error kind {e.kind}")
+
+
+class GpuTransport:
+    """In-process ring over p GPUs (rank r on devices[r]); threads play ranks,
+    exactly like the reference's InProcTransport (transport.py:150-177)."""
+
+    def __init__(self, world_size: int, latency_s: float = 0.0, byte_time_s: float = 0.0,
+                 timeout_s: float = DEFAULT_TIMEOUT_S, devices=None, max_elems: int = DEFAULT_MAX_ELEMS,
+                 ctas: int = 0):
+        if world_size < 1:
+            raise ConfigError("need at least one rank")
+        if latency_s or byte_time_s:
+            raise ConfigError("GPU transports do not inject synthetic delays (latency_s/byte_time_s)")
+        devices = list(range(world_size)) if devices is None else list(devices)
+        if len(devices) != world_size:
+            raise ConfigError("need one device per rank")
+        if len(set(devices)) != world_size:
+            raise ConfigError("GpuTransport needs a distinct GPU per rank; use EmulatedTransport "
+                              "to run more ranks than GPUs")
+        if torch.cuda.device_count() < max(devices) + 1:
+            raise ConfigError(f"{world_size} ranks need {max(devices) + 1} GPUs, "
+                              f"found {torch.cuda.device_count()}")
+        self.world_size = world_size
+        self.timeout_s = timeout_s
+        self.max_elems = max_elems
+        self._comms = [_comm_create(r, world_size, devices[r], max_elems) for r in range(world_size)]
+        for c in self._comms:
+            _lib.call("gp_comm_set_tuning", c, int(ctas), float(timeout_s))
+        if world_size > 1:
+            arr = (ctypes.c_void_p * world_size)(*[c.value for c in self._comms])
+            _lib.call("gp_comm_connect_local", arr, world_size)
+        self._eps = [GpuEndpoint(r, world_size, torch.device("cuda", devices[r]), self._comms[r],
+                                 timeout_s, transport=self) for r in range(world_size)]
+
+    def endpoint(self, rank: int) -> GpuEndpoint:
+        return self._eps[rank]
+
+    def close(self) -> None:
+        for c in self._comms:
+            _lib.load().gp_comm_destroy(c)
+        self._comms = []
+
+
+class _Rendezvous:
+    """Collects one call per virtual rank, launches the emulated ring once."""
+
+    def __init__(self, p: int, timeout_s: float):
+        self.p = p
+        self.timeout_s = timeout_s
+        self.cv = threading.Condition()
+        self.slots: dict[int, tuple] = {}
+        self.generation = 0
+        self.done_gen = -1
+        self.error: Exception | None = None
+
+
+class EmulatedEndpoint(GpuEndpoint):
+    def _launch(self, x, out, codec, iteration, stream):  # rendezvous instead of a lone launch
+        tr: EmulatedTransport = self._transport
+        tr._arrive(self.rank, x, out, codec, iteration)
+
+    def _check_errors(self, n: int) -> None:
+        tr: EmulatedTransport = self._transport
+        tr._finish(self.rank)
+
+    def _raw_stats(self) -> TrafficStats:
+        s = _lib.GpStats()
+        _lib.call("gp_get_stats", self._comm, self.rank, ctypes.byref(s))
+        return TrafficStats(int(s.messages), int(s.payload_bytes), int(s.frame_bytes))
+
+
+class EmulatedTransport:
+    """p ranks of the ring on one GPU, one cooperative launch per allreduce.
+
+    Ranks may call from p threads exactly like InProcTransport endpoints; the
+    last arrival launches `gp_allreduce_emulated` for everyone. Used to check
+    ring parity at p = 3/4/8 on a single B200 without separately launched
+    kernels that wait on each other."""
+
+    def __init__(self, world_size: int, latency_s: float = 0.0, byte_time_s: float = 0.0,
+                 timeout_s: float = DEFAULT_TIMEOUT_S, device: int = 0,
+                 max_elems: int = DEFAULT_MAX_ELEMS // 4, ctas: int = 0):
+        if latency_s or byte_time_s:
+            raise ConfigError("GPU transports do not inject synthetic delays")
+        self.world_size = world_size
+        self.timeout_s = timeout_s
+        self.device = torch.device("cuda", device)
+        h = ctypes.c_void_p()
+        _lib.call("gp_comm_create_emulated", world_size, device, max_elems, ctypes.byref(h))
+        self._comm = h
+        _lib.call("gp_comm_set_tuning", h, int(ctas), float(timeout_s))
+        self._rv = _Rendezvous(world_size, timeout_s)
+        self._eps = [EmulatedEndpoint(r, world_size, self.device, h, timeout_s, transport=self)
+                     for r in range(world_size)]
+        self._stream = torch.cuda.Stream(self.device)
+
+    def endpoint(self, rank: int) -> EmulatedEndpoint:
+        return self._eps[rank]
+
+    def _arrive(self, rank, x, out, codec, iteration):
+        rv = self._rv
+        with rv.cv:
+            gen = rv.generation
+            if rank in rv.slots:
+                raise CollectiveError(f"rank {rank} entered the same allreduce twice")
+            rv.slots[rank] = (x, out, int(codec), int(iteration), x.numel())
+            if len(rv.slots) == rv.p:
+                self._launch_all()
+                rv.generation += 1
+                rv.cv.notify_all()
+            else:
+                ok = rv.cv.wait_for(lambda: rv.generation != gen, timeout=rv.timeout_s)
+                if not ok:
+                    rv.slots.pop(rank, None)
+                    raise CollectiveError(f"reduce-scatter step 0 (rank {rank} <- {(rank - 1) % rv.p}): "
+                                          f"timed out after {rv.timeout_s:g}s")
+
+    def _launch_all(self):
+        rv = self._rv
+        args = [rv.slots[r] for r in range(rv.p)]
+        rv.slots = {}
+        ns = {a[4] for a in args}
+        codecs = {a[2] for a in args}
+        its = {a[3] for a in args}
+        rv.error = None
+        if len(ns) != 1 or len(codecs) != 1 or len(its) != 1:
+            rv.error = CollectiveError("reduce-scatter step 0: ranks disagree on vector length, codec or "
+                                       "iteration (unequal vector lengths across ranks?)")
+            return
+        n = ns.pop()
+        ins = (ctypes.c_void_p * rv.p)(*[a[0].data_ptr() for a in args])
+        outs = (ctypes.c_void_p * rv.p)(*[a[1].data_ptr() for a in args])
+        cur = torch.cuda.current_stream(self.device)
+        self._stream.wait_stream(cur)
+        for a in args:
+            a[0].record_stream(self._stream)
+            a[1].record_stream(self._stream)
+        _lib.call("gp_allreduce_emulated", self._comm, ins, outs, n, codecs.pop(), its.pop() & 0xFFFFFFFF,
+                  self._stream.cuda_stream)
+        self._stream.synchronize()
+        e = _lib.GpError()
+        _lib.call("gp_comm_poll_error", self._comm, ctypes.byref(e))
+        if e.kind:
+            rv.error = raise_for(e, rv.p, n, rv.timeout_s)
+
+    def _finish(self, rank):
+        if self._rv.error is not None:
+            raise self._rv.error
+
+    def close(self) -> None:
+        if self._comm:
+            _lib.load().gp_comm_destroy(self._comm)
+            self._comm = None
+
+
+class ProcessGroupTransport:
+    """One rank per process (torchrun), inboxes mapped through CUDA IPC.
+
+    The IPC handles travel over the existing torch.distributed process group
+    (any backend); after that no collective of torch.distributed is used on
+    the data path."""
+
+    @staticmethod
+    def endpoint(device: int | None = None, group=None, timeout_s: float = DEFAULT_TIMEOUT_S,
+                 max_elems: int = DEFAULT_MAX_ELEMS, ctas: int = 0) -> GpuEndpoint:
+        import torch.distributed as dist
+
+        rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        if device is None:
+            device = torch.cuda.current_device()
+        comm = _comm_create(rank, world, device, max_elems)
+        _lib.call("gp_comm_set_tuning", comm, int(ctas), float(timeout_s))
+        if world > 1:
+            h = ctypes.create_string_buffer(64)
+            _lib.call("gp_comm_ipc_handle", comm, h)
+            gathered = [None] * world
+            dist.all_gather_object(gathered, (h.raw, int(max_elems), int(device)), group=group)
+            if len({g[1] for g in gathered}) != 1:
+                raise ConfigError("all ranks must create the transport with the same max_elems")
+            if len({g[2] for g in gathered}) != world:
+                raise ConfigError("ProcessGroupTransport needs a distinct GPU per rank")
+            blob = b"".join(g[0] for g in gathered)
+            _lib.call("gp_comm_connect_ipc", comm, blob)
+            dist.barrier(group)
+        return GpuEndpoint(rank, world, torch.device("cuda", device), comm, timeout_s)

@@ -1,0 +1,173 @@
+"""GPU parity of the fused compressed ring AllReduce (csrc/ring.cu).
+
+* emulated ring (all p ranks in one cooperative launch on cuda:0) against
+  every golden case the real reference produced (p = 2, 3, 4, 8; 7 sizes;
+  4 magnitude variants; 3 codecs) and against the oracle at larger sizes;
+* the real multi-GPU ring (one GPU per rank, NVLink P2P) when the box has
+  >= 2 GPUs, same checks;
+* reference accounting (messages / payload / frame bytes) and error paths.
+Bar: bit-exact outputs on every rank (tests the reference's fold order).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import assert_bits_equal, run_ranks
+from oracle import ring as OR
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1811_03619_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(os.path.join(GOLD, "ring_golden.npz"))
+
+
+def golden_cases(gold, p):
+    for k in gold["keys"]:
+        k = str(k)
+        if k.startswith(f"p{p}_"):
+            yield k, int(k.split("_c")[1]), list(gold[k.rsplit("_c", 1)[0] + "_in"])
+
+
+def check_against_golden(P, tr, gold, p):
+    for k, codec, ins in golden_cases(gold, p):
+        def op(r, ep):
+            ep.reset_stats()
+            y = P.ring_allreduce(ins[r], r, p, ep, P.Codec(codec), iteration=3)
+            s = ep.stats
+            return y, (s.messages, s.payload_bytes, s.frame_bytes)
+
+        res = run_ranks(tr, op)
+        for r, (y, st) in enumerate(res):
+            assert_bits_equal(y, gold[k + "_out"], f"{k} rank {r}")
+        assert np.array_equal(np.array([st for _, st in res]), gold[k + "_stats"]), k
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_emulated_ring_matches_reference_golden(P, gold, p):
+    tr = P.EmulatedTransport(p, timeout_s=30.0, max_elems=1 << 14)
+    try:
+        check_against_golden(P, tr, gold, p)
+    finally:
+        tr.close()
+
+
+@pytest.mark.parametrize("p,n", [(2, (1 << 20) + 3), (4, (1 << 21) + 5), (8, 3_000_017), (3, 999_999)])
+def test_emulated_ring_large_vs_oracle(P, p, n):
+    g = np.random.default_rng((p, n))
+    ins = [(g.normal(0, 1, n) * 10.0 ** g.integers(-3, 3)).astype(np.float32) for _ in range(p)]
+    tr = P.EmulatedTransport(p, timeout_s=60.0, max_elems=n)
+    try:
+        for codec in P.Codec:
+            want = OR.ring_allreduce_all(ins, int(codec)).outputs[0]
+            xs = [torch.from_numpy(v).cuda() for v in ins]
+            res = run_ranks(tr, lambda r, ep: P.ring_allreduce(xs[r], r, p, ep, codec, iteration=7))
+            for r, y in enumerate(res):
+                assert y.is_cuda
+                assert_bits_equal(y.cpu().numpy(), want, f"p={p} n={n} {codec.name} rank {r}")
+    finally:
+        tr.close()
+
+
+def test_emulated_repeated_calls_reuse_inboxes(P):
+    p, n = 4, 50_000
+    tr = P.EmulatedTransport(p, timeout_s=30.0, max_elems=n)
+    g = np.random.default_rng(11)
+    try:
+        for it in range(25):
+            codec = P.Codec(it % 3)
+            m = int(g.integers(1, n))
+            ins = [g.normal(0, 1, m).astype(np.float32) for _ in range(p)]
+            want = OR.ring_allreduce_all(ins, int(codec)).outputs[0]
+            res = run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, p, ep, codec, iteration=it))
+            for y in res:
+                assert_bits_equal(y, want, f"iter {it} {codec.name} n={m}")
+    finally:
+        tr.close()
+
+
+def test_emulated_nonfinite_raises_codec_error(P):
+    p = 4
+    tr = P.EmulatedTransport(p, timeout_s=10.0, max_elems=4096)
+    ins = [np.ones(1000, np.float32) for _ in range(p)]
+    ins[2][500] = np.nan
+    try:
+        with pytest.raises(P.CodecError):
+            run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, p, ep, P.Codec.TRUNC16))
+        # the transport stays usable after a codec error
+        ins[2][500] = 1.0
+        res = run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, p, ep, P.Codec.TRUNC16))
+        assert np.all(res[0] == 4.0)
+    finally:
+        tr.close()
+
+
+def test_single_rank_is_identity(P):
+    tr = P.EmulatedTransport(1, max_elems=16)
+    vec = np.array([5.0, -1.0], np.float32)
+    out = P.ring_allreduce(vec, 0, 1, tr.endpoint(0), P.Codec.QUANT8)
+    assert np.array_equal(out, vec)
+    tr.close()
+
+
+def test_rank_mismatch_rejected(P):
+    tr = P.EmulatedTransport(2, max_elems=16)
+    with pytest.raises(P.CollectiveError):
+        P.ring_allreduce(np.ones(4, np.float32), 1, 2, tr.endpoint(0))
+    tr.close()
+
+
+# ------------------------------------------------------------ real multi-GPU
+
+multigpu = pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+
+
+@multigpu
+def test_p2p_ring_matches_reference_golden(P, gold):
+    p = 4 if NGPU >= 4 else 2
+    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=1 << 14)
+    try:
+        check_against_golden(P, tr, gold, p)
+    finally:
+        tr.close()
+
+
+@multigpu
+@pytest.mark.parametrize("n", [1, 4099, (1 << 22) + 3, 25_557_032])
+def test_p2p_ring_large_vs_oracle(P, n):
+    p = 4 if NGPU >= 4 else 2
+    g = np.random.default_rng(n)
+    ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
+    tr = P.GpuTransport(p, timeout_s=60.0, max_elems=n)
+    try:
+        for codec in P.Codec:
+            want = OR.ring_allreduce_all(ins, int(codec)).outputs[0]
+            xs = [torch.from_numpy(v).to(f"cuda:{r}") for r, v in enumerate(ins)]
+            res = run_ranks(tr, lambda r, ep: P.ring_allreduce(xs[r], r, p, ep, codec, iteration=1))
+            for r, y in enumerate(res):
+                assert y.device.index == r
+                assert_bits_equal(y.cpu().numpy(), want, f"n={n} {codec.name} rank {r}")
+    finally:
+        tr.close()
+
+
+@multigpu
+def test_p2p_timeout_produces_diagnostic(P):
+    tr = P.GpuTransport(2, timeout_s=0.5, max_elems=64)
+    try:
+        with pytest.raises(P.CollectiveError, match="reduce-scatter step 0"):
+            P.ring_allreduce(np.ones(8, np.float32), 0, 2, tr.endpoint(0))
+    finally:
+        tr.close()
