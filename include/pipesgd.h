@@ -21,6 +21,8 @@
  *   gp_roundtrip            engine.py:333 + :355/:400 decompress(compress(grad))
  *   gp_consume_update       engine.py:420-426 decompress -> engine.py:123-129
  *                           aggregate_mean -> models.py:198-204 sgd_update
+ *   gp_calib_p2p_copy       harness.py:552-557 beta probe (flood), on NVLink
+ *   gp_calib_pingpong       harness.py:547-550 alpha probe (1-byte ping), on NVLink
  *
  * Return value: GP_OK (0) or a GP_ERR_* code; gp_last_error_string() gives
  * the calling thread's last message. Failures detected on the device
@@ -104,6 +106,11 @@ int gp_roundtrip(int codec, const float* in, float* out, uint64_t n, gp_codec_st
                  void* stream);
 int gp_consume_update(float* params, int codec, const void* slot, const float* slot_scale,
                       uint64_t n, float lr, int world, void* stream);
+
+/* ---- calibration (timing-model alpha/beta on NVLink) ------------------- */
+int gp_calib_p2p_copy(void* dst, const void* src, uint64_t bytes, int ctas, int pull, void* stream);
+int gp_calib_pingpong(void* mine, void* theirs, int iters, int initiator, uint64_t base,
+                      void* ns_out /* device u64 */, void* stream);
 
 const char* gp_last_error_string(void);
 int gp_version(void);

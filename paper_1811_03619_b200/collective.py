@@ -64,7 +64,7 @@ def allreduce_into(x: torch.Tensor, out: torch.Tensor, endpoint: GpuEndpoint, co
     enqueue the fused ring on `stream` (default: current stream of the
     endpoint's device). Errors surface at `endpoint_wait`."""
     s = stream if stream is not None else torch.cuda.current_stream(endpoint.device)
-    endpoint._launch(x, out, as_codec(codec), iteration, s.cuda_stream)
+    endpoint._launch(x, out, as_codec(codec), iteration, s)
 
 
 def endpoint_wait(endpoint: GpuEndpoint, n: int, stream: torch.cuda.Stream | None = None) -> None:

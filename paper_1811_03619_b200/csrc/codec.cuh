@@ -16,6 +16,11 @@
 // are lifted by an exact power-of-two factor so 1/s stays finite and no
 // operand is subnormal. Results equal the reference bit for bit
 // (tests/test_gpu_codec.py vs tests/golden/codec_golden.npz).
+//
+// Wire groups: every lane moves exactly one 16-byte payload vector per step,
+// i.e. E = 16 / width elements (4 fp32 / 8 trunc16 halfwords / 16 quant8
+// codes), so a warp's payload access is 512 contiguous bytes — full 128-byte
+// lines on NVLink and in HBM.
 #pragma once
 
 #include "common.cuh"
@@ -58,8 +63,7 @@ __device__ __forceinline__ Q8 q8_make(float s) {
   return q;
 }
 
-// One element -> int8 code (as int). vmax==0 blocks never reach here with
-// nonzero x; x==0 (either sign) always yields 0.
+// One element -> int8 code (as int). x==0 (either sign) always yields 0.
 __device__ __forceinline__ int q8_encode(float x, const Q8& q) {
   if (q.zero) return x > 0.f ? 127 : (x < 0.f ? -127 : 0);
   const float a = __fmul_rn(fabsf(x), q.pre);
@@ -73,130 +77,149 @@ __device__ __forceinline__ int q8_encode(float x, const Q8& q) {
 }
 __device__ __forceinline__ float q8_decode(int code, float s) { return __fmul_rn((float)code, s); }
 
-// ---------------------------------------------------------------- wire groups
-// A group is 8 consecutive elements starting at a global index that is a
-// multiple of 8; its wire image is 32 / 16 / 8 bytes for none / trunc16 /
-// quant8, so every full group moves with aligned vector accesses.
+// ----------------------------------------------------------- wire groups
 
-template <int C> struct Packed;
-template <> struct Packed<kNone> { uint32_t w[8]; static constexpr int kWidth = 4; };
-template <> struct Packed<kTrunc16> { uint32_t w[4]; static constexpr int kWidth = 2; };
-template <> struct Packed<kQuant8> { uint32_t w[2]; static constexpr int kWidth = 1; };
+template <int C> struct CodecT;
+template <> struct CodecT<kNone> { static constexpr int W = 4, E = 4; };
+template <> struct CodecT<kTrunc16> { static constexpr int W = 2, E = 8; };
+template <> struct CodecT<kQuant8> { static constexpr int W = 1, E = 16; };
 
-template <int C>
-__device__ __forceinline__ Packed<C> encode8(const F8& v, const Q8& q, int& bad) {
-  Packed<C> p;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) bad |= nonfinite(v.v[i]);
-  if constexpr (C == kNone) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) p.w[i] = __float_as_uint(v.v[i]);
-  } else if constexpr (C == kTrunc16) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) p.w[i] = t16_encode(v.v[2 * i]) | (t16_encode(v.v[2 * i + 1]) << 16);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      uint32_t w = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) w |= ((uint32_t)(q8_encode(v.v[4 * i + k], q) & 0xFF)) << (8 * k);
-      p.w[i] = w;
-    }
-  }
-  return p;
+template <int E>
+struct FV {
+  float v[E];
+};
+
+__device__ __forceinline__ uint32_t wget(const uint4& p, int i) {
+  return i == 0 ? p.x : i == 1 ? p.y : i == 2 ? p.z : p.w;
 }
 
 template <int C>
-__device__ __forceinline__ F8 decode8(const Packed<C>& p, float s) {
-  F8 v;
+__device__ __forceinline__ uint4 encode_v(const FV<CodecT<C>::E>& v, const Q8& q, int& bad) {
+  constexpr int E = CodecT<C>::E;
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
   if constexpr (C == kNone) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v.v[i] = __uint_as_float(p.w[i]);
+    for (int i = 0; i < 4; ++i) w[i] = __float_as_uint(v.v[i]);
+  } else if constexpr (C == kTrunc16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = t16_encode(v.v[2 * i]) | (t16_encode(v.v[2 * i + 1]) << 16);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x |= ((uint32_t)(q8_encode(v.v[4 * i + k], q) & 0xFF)) << (8 * k);
+      w[i] = x;
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int C>
+__device__ __forceinline__ FV<CodecT<C>::E> decode_v(const uint4& p, float s) {
+  FV<CodecT<C>::E> v;
+  const uint32_t w[4] = {p.x, p.y, p.z, p.w};
+  if constexpr (C == kNone) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v.v[i] = __uint_as_float(w[i]);
   } else if constexpr (C == kTrunc16) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      v.v[2 * i] = t16_decode(p.w[i] & 0xFFFFu);
-      v.v[2 * i + 1] = t16_decode(p.w[i] >> 16);
+      v.v[2 * i] = t16_decode(w[i] & 0xFFFFu);
+      v.v[2 * i + 1] = t16_decode(w[i] >> 16);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int code = (int)(int8_t)((p.w[i >> 2] >> (8 * (i & 3))) & 0xFF);
-      v.v[i] = q8_decode(code, s);
-    }
+    for (int i = 0; i < 16; ++i) v.v[i] = q8_decode((int)(int8_t)((w[i >> 2] >> (8 * (i & 3))) & 0xFF), s);
   }
   return v;
 }
 
-// Byte address of group element 0 inside a slot: rel0 = g0 - floor8(block start).
-template <int C>
-__device__ __forceinline__ Packed<C> load_packed(const uint8_t* slot, uint64_t rel0, int vlo, int vhi) {
-  Packed<C> p;
-  const uint8_t* base = slot + rel0 * Packed<C>::kWidth;
-  if (vlo == 0 && vhi == 8) {
-    if constexpr (C == kNone) {
-      const uint4* q = reinterpret_cast<const uint4*>(base);
-      uint4 a = __ldcg(q), b = __ldcg(q + 1);
-      p.w[0] = a.x; p.w[1] = a.y; p.w[2] = a.z; p.w[3] = a.w;
-      p.w[4] = b.x; p.w[5] = b.y; p.w[6] = b.z; p.w[7] = b.w;
-    } else if constexpr (C == kTrunc16) {
-      uint4 a = __ldcg(reinterpret_cast<const uint4*>(base));
-      p.w[0] = a.x; p.w[1] = a.y; p.w[2] = a.z; p.w[3] = a.w;
-    } else {
-      uint2 a = __ldcg(reinterpret_cast<const uint2*>(base));
-      p.w[0] = a.x; p.w[1] = a.y;
+// fp32 values x[g0 .. g0+E) restricted to [lo, hi); outside lanes read 0.
+// NC=true uses the read-only path (inputs not written by this launch).
+template <int E, bool NC = true>
+__device__ __forceinline__ FV<E> load_fv(const float* x, uint64_t g0, uint64_t lo, uint64_t hi) {
+  FV<E> r;
+  if (lo <= g0 && g0 + E <= hi) {
+    const float4* p = reinterpret_cast<const float4*>(x + g0);
+#pragma unroll
+    for (int k = 0; k < E / 4; ++k) {
+      const float4 a = NC ? __ldg(p + k) : __ldcg(p + k);
+      r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < (int)(sizeof(p.w) / 4); ++i) p.w[i] = 0;
-    for (int i = vlo; i < vhi; ++i) {
-      if constexpr (C == kNone) {
-        p.w[i] = __ldcg(reinterpret_cast<const unsigned int*>(base) + i);
-      } else if constexpr (C == kTrunc16) {
-        const uint32_t h = __ldcg(reinterpret_cast<const unsigned short*>(base) + i);
-        p.w[i >> 1] |= h << (16 * (i & 1));
-      } else {
-        const uint32_t b = (uint8_t)__ldcg(reinterpret_cast<const signed char*>(base) + i);
-        p.w[i >> 2] |= b << (8 * (i & 3));
-      }
-    }
+    for (int i = 0; i < E; ++i)
+      r.v[i] = (g0 + i >= lo && g0 + i < hi) ? (NC ? __ldg(x + g0 + i) : __ldcg(x + g0 + i)) : 0.f;
   }
-  return p;
+  return r;
 }
 
-// Store (possibly to a peer GPU over NVLink) only lanes [vlo, vhi).
-template <int C>
-__device__ __forceinline__ void store_packed(uint8_t* slot, uint64_t rel0, int vlo, int vhi,
-                                             const Packed<C>& p) {
-  uint8_t* base = slot + rel0 * Packed<C>::kWidth;
-  if (vlo == 0 && vhi == 8) {
-    if constexpr (C == kNone) {
-      uint4* q = reinterpret_cast<uint4*>(base);
-      __stcg(q, make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]));
-      __stcg(q + 1, make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]));
-    } else if constexpr (C == kTrunc16) {
-      __stcg(reinterpret_cast<uint4*>(base), make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]));
-    } else {
-      __stcg(reinterpret_cast<uint2*>(base), make_uint2(p.w[0], p.w[1]));
-    }
+template <int E>
+__device__ __forceinline__ void store_fv(float* x, uint64_t g0, uint64_t lo, uint64_t hi, const FV<E>& r) {
+  if (lo <= g0 && g0 + E <= hi) {
+    float4* p = reinterpret_cast<float4*>(x + g0);
+#pragma unroll
+    for (int k = 0; k < E / 4; ++k) p[k] = make_float4(r.v[4 * k], r.v[4 * k + 1], r.v[4 * k + 2], r.v[4 * k + 3]);
   } else {
-    for (int i = vlo; i < vhi; ++i) {
-      if constexpr (C == kNone) {
-        reinterpret_cast<uint32_t*>(base)[i] = p.w[i];
-      } else if constexpr (C == kTrunc16) {
-        reinterpret_cast<uint16_t*>(base)[i] = (uint16_t)(p.w[i >> 1] >> (16 * (i & 1)));
-      } else {
-        base[i] = (uint8_t)(p.w[i >> 2] >> (8 * (i & 3)));
-      }
-    }
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (g0 + i >= lo && g0 + i < hi) x[g0 + i] = r.v[i];
   }
 }
 
-__device__ __forceinline__ uint32_t absmax8_bits(const F8& v) {
+// Payload vector of the group whose first element is `rel0` elements past
+// the slot origin; only elements [vlo, vhi) of the group exist.
+template <int C>
+__device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, int vlo, int vhi) {
+  constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
+  const uint8_t* base = slot + rel0 * W;
+  if (vlo == 0 && vhi == E) return __ldcg(reinterpret_cast<const uint4*>(base));
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (int i = vlo; i < vhi; ++i) {
+    uint32_t e;
+    if constexpr (W == 4) e = __ldcg(reinterpret_cast<const unsigned int*>(base) + i);
+    else if constexpr (W == 2) e = __ldcg(reinterpret_cast<const unsigned short*>(base) + i);
+    else e = (uint8_t)__ldcg(reinterpret_cast<const signed char*>(base) + i);
+    const int bit = (i * W * 8) & 31;
+    w[(i * W) >> 2] |= e << bit;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int C>
+__device__ __forceinline__ void store_pay(uint8_t* slot, uint64_t rel0, int vlo, int vhi, const uint4& p) {
+  constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
+  uint8_t* base = slot + rel0 * W;
+  if (vlo == 0 && vhi == E) {
+    __stcg(reinterpret_cast<uint4*>(base), p);
+    return;
+  }
+  for (int i = vlo; i < vhi; ++i) {
+    const uint32_t word = wget(p, (i * W) >> 2);
+    const int bit = (i * W * 8) & 31;
+    if constexpr (W == 4) reinterpret_cast<uint32_t*>(base)[i] = word;
+    else if constexpr (W == 2) reinterpret_cast<uint16_t*>(base)[i] = (uint16_t)(word >> bit);
+    else base[i] = (uint8_t)(word >> bit);
+  }
+}
+
+template <int E>
+__device__ __forceinline__ uint32_t absmax_bits(const FV<E>& v) {
   uint32_t m = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) m = max(m, __float_as_uint(v.v[i]) & 0x7FFFFFFFu);
+  for (int i = 0; i < E; ++i) m = max(m, __float_as_uint(v.v[i]) & 0x7FFFFFFFu);
   return m;
+}
+
+template <int E>
+__device__ __forceinline__ FV<E> add_v(const FV<E>& a, const FV<E>& b) {
+  FV<E> r;
+#pragma unroll
+  for (int i = 0; i < E; ++i) r.v[i] = __fadd_rn(a.v[i], b.v[i]);
+  return r;
 }
 
 }  // namespace gp

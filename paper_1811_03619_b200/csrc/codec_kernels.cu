@@ -34,22 +34,26 @@ uint32_t grid_for(uint64_t n) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const uint64_t groups = (n + 7) / 8;
+  const uint64_t groups = (n + 3) / 4;
   const uint64_t want = (groups + kT - 1) / kT;
   const uint64_t cap = (uint64_t)sms * 8;
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
+
+#define GROUP_LOOP(E) \
+  for (uint64_t g0 = (uint64_t)(E) * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; \
+       g0 += (uint64_t)(E) * kT * gridDim.x)
 
 __global__ void __launch_bounds__(kT) absmax_kernel(const float* __restrict__ x, uint64_t n,
                                                     gp_codec_status* st) {
   __shared__ uint32_t red[kT / 32];
   uint32_t m = 0;
   int bad = 0;
-  for (uint64_t g0 = 8ull * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; g0 += 8ull * kT * gridDim.x) {
-    const F8 v = load_f8(x, g0, g0, min(n, g0 + 8));
-    m = max(m, absmax8_bits(v));
+  GROUP_LOOP(4) {
+    const FV<4> v = load_fv<4>(x, g0, 0, n);
+    m = max(m, absmax_bits(v));
 #pragma unroll
-    for (int i = 0; i < 8; ++i) bad |= nonfinite(v.v[i]);
+    for (int i = 0; i < 4; ++i) bad |= nonfinite(v.v[i]);
   }
   m = cta_max_u32<kT>(m, red);
   bad = __syncthreads_or(bad);
@@ -60,20 +64,22 @@ __global__ void __launch_bounds__(kT) absmax_kernel(const float* __restrict__ x,
 }
 
 template <int C>
+__device__ __forceinline__ Q8 status_scale(gp_codec_status* st) {
+  Q8 q = q8_make(0.f);
+  if constexpr (C == kQuant8) q = q8_make(q8_scale(__uint_as_float(*(volatile uint32_t*)&st->absmax_bits)));
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->scale = q.s;
+  return q;
+}
+
+template <int C>
 __global__ void __launch_bounds__(kT) encode_kernel(const float* __restrict__ x, uint64_t n,
                                                     uint8_t* payload, gp_codec_status* st) {
-  Q8 q = q8_make(0.f);
-  if constexpr (C == kQuant8) {
-    q = q8_make(q8_scale(__uint_as_float(*(volatile uint32_t*)&st->absmax_bits)));
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->scale = q.s;
-  } else {
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->scale = 0.f;
-  }
+  constexpr int E = CodecT<C>::E;
+  const Q8 q = status_scale<C>(st);
   int bad = 0;
-  for (uint64_t g0 = 8ull * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; g0 += 8ull * kT * gridDim.x) {
-    const uint64_t hi = min(n, g0 + 8);
-    const Packed<C> pk = encode8<C>(load_f8(x, g0, g0, hi), q, bad);
-    store_packed<C>(payload, g0, 0, (int)(hi - g0), pk);
+  GROUP_LOOP(E) {
+    const uint4 pk = encode_v<C>(load_fv<E>(x, g0, 0, n), q, bad);
+    store_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0), pk);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
@@ -81,26 +87,22 @@ __global__ void __launch_bounds__(kT) encode_kernel(const float* __restrict__ x,
 template <int C>
 __global__ void __launch_bounds__(kT) decode_kernel(const uint8_t* payload, const float* scale, uint64_t n,
                                                     float* out) {
+  constexpr int E = CodecT<C>::E;
   const float s = (C == kQuant8) ? *scale : 0.f;
-  for (uint64_t g0 = 8ull * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; g0 += 8ull * kT * gridDim.x) {
-    const uint64_t hi = min(n, g0 + 8);
-    store_f8(out, g0, g0, hi, decode8<C>(load_packed<C>(payload, g0, 0, (int)(hi - g0)), s));
+  GROUP_LOOP(E) {
+    store_fv<E>(out, g0, 0, n, decode_v<C>(load_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0)), s));
   }
 }
 
 template <int C>
 __global__ void __launch_bounds__(kT) roundtrip_kernel(const float* __restrict__ x, uint64_t n, float* out,
                                                        gp_codec_status* st) {
-  Q8 q = q8_make(0.f);
-  if constexpr (C == kQuant8) {
-    q = q8_make(q8_scale(__uint_as_float(*(volatile uint32_t*)&st->absmax_bits)));
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->scale = q.s;
-  }
+  constexpr int E = CodecT<C>::E;
+  const Q8 q = status_scale<C>(st);
   int bad = 0;
-  for (uint64_t g0 = 8ull * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; g0 += 8ull * kT * gridDim.x) {
-    const uint64_t hi = min(n, g0 + 8);
-    const Packed<C> pk = encode8<C>(load_f8(x, g0, g0, hi), q, bad);
-    store_f8(out, g0, g0, hi, decode8<C>(pk, q.s));
+  GROUP_LOOP(E) {
+    const uint4 pk = encode_v<C>(load_fv<E>(x, g0, 0, n), q, bad);
+    store_fv<E>(out, g0, 0, n, decode_v<C>(pk, q.s));
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
@@ -108,18 +110,18 @@ __global__ void __launch_bounds__(kT) roundtrip_kernel(const float* __restrict__
 template <int C>
 __global__ void __launch_bounds__(kT) consume_update_kernel(float* w, const uint8_t* slot, const float* scale,
                                                             uint64_t n, float lr, int p) {
+  constexpr int E = CodecT<C>::E;
   const float s = (C == kQuant8) ? *scale : 0.f;
   const float fp = (float)p;
-  for (uint64_t g0 = 8ull * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; g0 += 8ull * kT * gridDim.x) {
-    const uint64_t hi = min(n, g0 + 8);
-    const F8 g = decode8<C>(load_packed<C>(slot, g0, 0, (int)(hi - g0)), s);
-    F8 v = load_f8_cg(w, g0, g0, hi);
+  GROUP_LOOP(E) {
+    const FV<E> g = decode_v<C>(load_pay<C>(slot, g0, 0, (int)(min(n, g0 + E) - g0)), s);
+    FV<E> v = load_fv<E, false>(w, g0, 0, n);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < E; ++i) {
       const float gm = p == 1 ? g.v[i] : __fdiv_rn(g.v[i], fp);
       v.v[i] = __fsub_rn(v.v[i], __fmul_rn(lr, gm));
     }
-    store_f8(w, g0, g0, hi, v);
+    store_fv<E>(w, g0, 0, n, v);
   }
 }
 

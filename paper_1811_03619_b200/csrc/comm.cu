@@ -5,6 +5,7 @@
 // endpoint bookkeeping (rank, world, timeout, stats) stays.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -44,8 +45,8 @@ Layout make_layout(int p, uint64_t max_elems) {
   Layout L{};
   const uint64_t maxblk = (max_elems + p - 1) / p;
   L.nslot = (uint32_t)(2 * p - 1);
-  L.slot_bytes = round_up((maxblk + 16) * 4, 256);
-  L.max_chunks = (uint32_t)((maxblk + 8 + kMinChunk - 1) / kMinChunk + 1);
+  L.slot_bytes = round_up((maxblk + 32) * 4, 256);
+  L.max_chunks = (uint32_t)((maxblk + 16 + kMinChunk - 1) / kMinChunk + 1);
   L.off_ctl = 0;
   L.off_err = 4096;
   L.off_hdr = 4096 + 256;
@@ -89,7 +90,7 @@ int alloc_inbox(gp_comm* c, int i) {
 int default_ctas(int device) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  return std::max(1, std::min(64, sms / 2));
+  return std::max(1, sms);
 }
 
 void count_message(gp_stats& s, int codec, uint64_t len) {
@@ -115,9 +116,15 @@ void account(gp_stats& s, int rank, int p, uint64_t n, int codec) {
 }
 
 uint32_t pick_chunk(uint64_t n, int p, int G) {
-  const uint64_t maxblk = (n + p - 1) / p + 8;
-  uint64_t ch = round_up((maxblk + G - 1) / G, kMinChunk);
-  ch = std::max<uint64_t>(kMinChunk, std::min<uint64_t>(kMaxChunk, ch));
+  static const uint64_t max_chunk = [] {
+    const char* e = std::getenv("PIPESGD_MAX_CHUNK");
+    const uint64_t v = e ? std::strtoull(e, nullptr, 10) : kMaxChunk;
+    return std::max<uint64_t>(kMinChunk, v / kMinChunk * kMinChunk);
+  }();
+  const uint64_t maxblk = (n + p - 1) / p + 16;
+  const uint64_t workers = (uint64_t)G * kRingWarps;
+  uint64_t ch = round_up((maxblk + workers - 1) / workers, kMinChunk);
+  ch = std::max<uint64_t>(kMinChunk, std::min<uint64_t>(max_chunk, ch));
   return (uint32_t)ch;
 }
 
@@ -173,8 +180,8 @@ int gp_comm_create_emulated(int world, int device, uint64_t max_elems, gp_comm**
   c->L = make_layout(world, c->max_elems);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  // all p x G CTAs must be co-resident (2 x 512-thread CTAs per SM)
-  c->G = std::max(1, std::min(16, (2 * sms) / world));
+  // all p x G CTAs must be co-resident (1 x 512-thread CTA per SM)
+  c->G = std::max(1, std::min(16, sms / world));
   for (int i = 0; i < world; ++i) {
     int rc = alloc_inbox(c, i);
     if (rc) { for (int k = 0; k < i; ++k) cudaFree(c->inbox[k]); delete c; return rc; }
@@ -254,7 +261,7 @@ int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
   if (ctas > 0) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    const int cap = c->nlocal == 1 ? sms : std::max(1, (2 * sms) / c->nlocal);
+    const int cap = std::max(1, sms / c->nlocal);  // every CTA of the launch co-resident
     c->G = std::min(ctas, cap);
   }
   if (timeout_s > 0) c->timeout_s = timeout_s;
@@ -311,7 +318,7 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint6
   cudaError_t e;
   launch_ring(P, c->nlocal, st, &e);
   if (e != cudaSuccess) return cuda_fail(e, "ring kernel launch");
-  if (codec == GP_CODEC_QUANT8) c->bar_total += (unsigned long long)p * c->G;
+  if (codec == GP_CODEC_QUANT8) c->bar_total += (unsigned long long)p * c->G * kRingWarps;
   for (int i = 0; i < c->nlocal; ++i) account(c->stats[i], P.rk[i].rank, p, n, codec);
   return GP_OK;
 }

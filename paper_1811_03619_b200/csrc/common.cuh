@@ -107,53 +107,4 @@ __device__ __forceinline__ int cta_or(int v, int* smem) {
   return r;
 }
 
-// 8 consecutive fp32 values whose first global index is a multiple of 8.
-struct F8 {
-  float v[8];
-};
-
-// Load x[g0 .. g0+8) restricted to [lo, hi); lanes outside read as 0.
-__device__ __forceinline__ F8 load_f8(const float* __restrict__ x, uint64_t g0, uint64_t lo,
-                                      uint64_t hi) {
-  F8 r;
-  if (lo == g0 && hi == g0 + 8) {
-    const float4* p = reinterpret_cast<const float4*>(x + g0);
-    float4 a = __ldg(p), b = __ldg(p + 1);
-    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
-    r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r.v[i] = (g0 + i >= lo && g0 + i < hi) ? x[g0 + i] : 0.f;
-  }
-  return r;
-}
-
-// Same, but through L2 only (data produced earlier in this launch).
-__device__ __forceinline__ F8 load_f8_cg(const float* x, uint64_t g0, uint64_t lo, uint64_t hi) {
-  F8 r;
-  if (lo == g0 && hi == g0 + 8) {
-    const float4* p = reinterpret_cast<const float4*>(x + g0);
-    float4 a = __ldcg(p), b = __ldcg(p + 1);
-    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
-    r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r.v[i] = (g0 + i >= lo && g0 + i < hi) ? __ldcg(x + g0 + i) : 0.f;
-  }
-  return r;
-}
-
-__device__ __forceinline__ void store_f8(float* x, uint64_t g0, uint64_t lo, uint64_t hi,
-                                         const F8& r) {
-  if (lo == g0 && hi == g0 + 8) {
-    float4* p = reinterpret_cast<float4*>(x + g0);
-    p[0] = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
-    p[1] = make_float4(r.v[4], r.v[5], r.v[6], r.v[7]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (g0 + i >= lo && g0 + i < hi) x[g0 + i] = r.v[i];
-  }
-}
-
 }  // namespace gp

@@ -8,28 +8,35 @@
 // so block b is the left fold s_0 = x_b, s_k = fl(x_{b+k} + D(C(s_{k-1})))
 // starting at rank b, and out[b] = D(C(s_{p-1})) on every rank.
 //
-// B200 mapping. One cooperative launch per rank per call, G CTAs of 512
-// threads. A block is cut into chunks of `chunk` elements aligned to
-// multiples of 8 global indices; chunk c of every block belongs to CTA c%G
-// on every rank, so each chunk flows around the ring independently:
-//   wait flag(slot s, chunk c) -> decode inbox + add local -> encode ->
-//   st.global into succ's inbox over NVLink -> st.release.sys succ's flag.
+// B200 mapping. One cooperative launch per rank per call: G CTAs x 16 warps.
+// Every WARP is an independent worker. A ring block is cut into chunks of
+// `chunk` elements (multiple of 1024, origin = block start rounded down to
+// 16); chunk c of every block belongs to warp c % (16G) on every rank, so
+// each chunk flows around the ring on its own:
+//   lane 0 acquires flag(slot s, chunk c) -> the warp streams the chunk in
+//   1024-element batches (each lane one 16-byte payload vector per group:
+//   4 fp32 / 8 trunc16 / 16 quant8 elements) -> decode inbox + add local ->
+//   encode -> st.global into succ's inbox over NVLink -> __syncwarp ->
+//   lane 0: fence.acq_rel.sys + st.release.sys succ's flag.
+// No CTA-wide barrier sits on the data path, so a warp waiting on its fence
+// or flag never stalls the other 15 warps of its SM.
 // quant8 needs the block-wide max before any code can be emitted
-// (compression.py:129-132), so each of its hops is two passes around a
-// rank-local barrier: pass A folds and reduces the max (partial sums parked
-// in `out`, L2-resident), pass B encodes and pushes. The allgather is a
-// direct owner->all-peers push over NVSwitch (same bytes the ring would
-// forward, one hop instead of p-1).
-// Emulation: with nlocal == p the same kernel runs all ranks of the ring on
-// one GPU inside one cooperative launch (CTA group = rank), used for parity
-// tests at p > #GPUs without separately-launched kernels that wait on each
-// other.
+// (compression.py:129-132): each of its hops is pass A (fold, park the
+// partial sum in `out`, reduce the max), a rank-wide barrier carrying the
+// max (per-warp atomics on the rank's control block), then pass B (encode
+// with the block scale, push). The allgather is a direct owner->all-peers
+// push over NVSwitch (the bytes the ring would forward, one hop not p-1).
+// Emulation: with nlocal == p the same kernel runs all p ranks on one GPU
+// in one cooperative launch (CTA group = rank) for parity tests at p > #GPUs.
 #include "codec.cuh"
 #include "ring.cuh"
 
 namespace gp {
 
 namespace {
+
+constexpr int kWarps = kRingThreads / 32;
+constexpr uint64_t kBatch = 1024;  // elements per warp per batch (32 lanes x U x E)
 
 struct Blk {
   uint64_t start, len, A;
@@ -39,16 +46,12 @@ struct Blk {
 __device__ __forceinline__ Blk get_blk(const RingParams& P, int b) {
   Blk k;
   block_range(P.n, P.p, b, k.start, k.len);
-  k.A = k.start & ~7ull;
+  k.A = k.start & ~15ull;
   k.nch = k.len ? (uint32_t)((k.start + k.len - k.A + P.chunk - 1) / P.chunk) : 0u;
   return k;
 }
 
-struct Sh {
-  uint32_t red[kRingThreads / 32];
-  int ok;
-  float scale;
-};
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ uint64_t* flag_ptr(uint8_t* inbox, const Layout& L, int slot, uint32_t c) {
   return reinterpret_cast<uint64_t*>(inbox + L.off_flags) + (uint64_t)slot * L.max_chunks + c;
@@ -69,15 +72,19 @@ __device__ void broadcast_abort(const RingParams& P, const RankCtx& R) {
   fence_sys();
 }
 
-// Thread 0 spins until *f >= seq. Returns false on timeout or abort.
+__device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
+  return *(volatile unsigned long long*)&ctl->abort >= P.seq;
+}
+
+// Lane 0 spins until *f >= seq. Returns false on timeout or abort.
 __device__ bool spin_flag(const uint64_t* f, const RingParams& P, const RankCtx& R, Ctl* ctl,
                           ErrWord* err, int phase, int step, int block) {
   if (ld_acquire_sys(f) >= P.seq) return true;
   const uint64_t t0 = globaltimer();
   for (uint32_t it = 1;; ++it) {
     if (ld_acquire_sys(f) >= P.seq) return true;
-    if ((it & 255u) == 0) {
-      if (*(volatile unsigned long long*)&ctl->abort >= P.seq) {
+    if ((it & 127u) == 0) {
+      if (aborted(P, ctl)) {
         latch_error(err, kErrTimeout, phase, step, block, R.rank, 1 /* peer aborted */);
         return false;
       }
@@ -90,107 +97,139 @@ __device__ bool spin_flag(const uint64_t* f, const RingParams& P, const RankCtx&
   }
 }
 
-// All threads: wait for (slot, chunk) of this rank's inbox, validate the
-// slot header like collective.py:_expect (:52-64, :109-114), fetch scale.
-__device__ bool await_chunk(Sh& sh, const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err,
-                            int slot, uint32_t c, int phase, int step, int block, uint64_t len,
-                            float& scale) {
-  if (threadIdx.x == 0) {
-    bool ok = spin_flag(flag_ptr(R.inbox, P.L, slot, c), P, R, ctl, err, phase, step, block);
+// Warp: wait for (slot, chunk) of this rank's inbox, validate the slot
+// header like collective.py:_expect (:52-64, :109-114), fetch the scale.
+__device__ bool warp_await(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err, int slot,
+                           uint32_t c, int phase, int step, int block, uint64_t len, float& scale) {
+  int ok = 1;
+  float s = 0.f;
+  if (lane_id() == 0) {
+    ok = spin_flag(flag_ptr(R.inbox, P.L, slot, c), P, R, ctl, err, phase, step, block);
     if (ok) {
       const SlotHdr* h = hdr_ptr(R.inbox, P.L, slot);
       const uint32_t hb = __ldcg(&h->block), hi = __ldcg(&h->iteration), hn = __ldcg(&h->n_elems);
       if (hb != (uint32_t)block || hi != P.iteration || hn != (uint32_t)len) {
         latch_error(err, kErrHeader, phase, step, block, R.rank, (int)hn);
         broadcast_abort(P, R);
-        ok = false;
+        ok = 0;
       }
-      sh.scale = __ldcg(&h->scale);
+      s = __ldcg(&h->scale);
     }
-    sh.ok = ok;
   }
-  __syncthreads();
-  scale = sh.scale;
-  return sh.ok;
+  __syncwarp();
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  scale = __shfl_sync(0xffffffffu, s, 0);
+  return ok;
 }
 
-// All threads: after this CTA's payload stores to `dst_inbox`, write the
-// slot header and release the chunk flag at system scope.
-__device__ __forceinline__ void publish(const RingParams& P, uint8_t* dst_inbox, int slot, uint32_t c,
-                                        int block, uint64_t len, float scale) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    SlotHdr* h = hdr_ptr(dst_inbox, P.L, slot);
-    h->seq = P.seq;
-    h->iteration = P.iteration;
-    h->block = (uint32_t)block;
-    h->n_elems = (uint32_t)len;
-    h->scale = scale;
-    fence_sys();
-    st_release_sys(flag_ptr(dst_inbox, P.L, slot, c), P.seq);
+__device__ __forceinline__ void write_hdr(const RingParams& P, uint8_t* dst, int slot, int block,
+                                          uint64_t len, float scale) {
+  SlotHdr* h = hdr_ptr(dst, P.L, slot);
+  h->seq = P.seq;
+  h->iteration = P.iteration;
+  h->block = (uint32_t)block;
+  h->n_elems = (uint32_t)len;
+  h->scale = scale;
+}
+
+// Warp: after this warp's payload stores to `dst`, publish the slot header
+// and release the chunk flag at system scope.
+__device__ __forceinline__ void warp_publish(const RingParams& P, uint8_t* dst, int slot, uint32_t c,
+                                             int block, uint64_t len, float scale) {
+  __syncwarp();
+  if (lane_id() == 0) {
+    write_hdr(P, dst, slot, block, len, scale);
+    st_release_sys(flag_ptr(dst, P.L, slot, c), P.seq);  // release: orders the warp's stores
   }
 }
 
-// quant8: rank-local barrier across the G CTAs of one rank, combined with
-// the block max. Returns false on abort/timeout.
-__device__ bool barrier_max(Sh& sh, const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err,
-                            int k, uint32_t mymax, float& vmax, int step) {
-  const uint32_t m = cta_max_u32<kRingThreads>(mymax, sh.red);
-  if (threadIdx.x == 0) {
+// Warp: publish chunk c of the owned block to every peer's allgather slot.
+__device__ __forceinline__ void warp_publish_all(const RingParams& P, const RankCtx& R, int b, uint32_t c,
+                                                 uint64_t len, float scale) {
+  __syncwarp();
+  if (lane_id() == 0) {
+    for (int d = 1; d < P.p; ++d) write_hdr(P, R.peer[(R.rank + d) % P.p], ag_slot(P.p, b), b, len, scale);
+    fence_sys();  // one system fence, then relaxed-cost releases to every peer
+    for (int d = 1; d < P.p; ++d)
+      st_release_sys(flag_ptr(R.peer[(R.rank + d) % P.p], P.L, ag_slot(P.p, b), c), P.seq);
+  }
+}
+
+// quant8: rank-wide barrier over all 16G warps of one rank carrying the
+// block max. Returns false on abort/timeout.
+__device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err, int k,
+                                 uint32_t mymax, float& vmax, int step) {
+  const uint32_t m = warp_max_u32(mymax);
+  int ok = 1;
+  float v = 0.f;
+  if (lane_id() == 0) {
     atomicMax(&ctl->maxslot[k], ((unsigned long long)P.seq << 32) | m);
     __threadfence();
     atomicAdd(&ctl->bar, 1ull);
-    const unsigned long long target = P.bar_base + (unsigned long long)(k + 1) * P.G;
-    bool ok = true;
+    const unsigned long long target = P.bar_base + (unsigned long long)(k + 1) * P.G * kWarps;
     const uint64_t t0 = globaltimer();
     for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->bar)) < target; ++it) {
-      if ((it & 255u) == 0) {
-        if (*(volatile unsigned long long*)&ctl->abort >= P.seq) { ok = false; break; }
+      __nanosleep(64);
+      if ((it & 63u) == 0) {
+        if (aborted(P, ctl)) { ok = 0; break; }
         if (globaltimer() - t0 > P.timeout_ns) {
           latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, 0);
           broadcast_abort(P, R);
-          ok = false;
+          ok = 0;
           break;
         }
       }
     }
-    const unsigned long long v = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->maxslot[k]));
-    sh.scale = ((uint32_t)(v >> 32) == P.seq) ? __uint_as_float((uint32_t)v) : 0.f;
-    sh.ok = ok;
+    const unsigned long long w = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->maxslot[k]));
+    v = ((uint32_t)(w >> 32) == P.seq) ? __uint_as_float((uint32_t)w) : 0.f;
   }
-  __syncthreads();
-  vmax = sh.scale;
-  return sh.ok;
+  __syncwarp();
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  vmax = __shfl_sync(0xffffffffu, v, 0);
+  return ok;
 }
 
-__device__ __forceinline__ F8 add8(const F8& a, const F8& b) {
-  F8 r;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) r.v[i] = __fadd_rn(a.v[i], b.v[i]);
-  return r;
-}
-
-// Iterate the 8-element groups of chunk c of block B owned by this thread.
-template <typename Fn>
-__device__ __forceinline__ void for_groups(const RingParams& P, const Blk& B, uint32_t c, Fn&& fn) {
+// Iterate this lane's groups of chunk c of block B in 1024-element batches;
+// all loads of a batch are issued before any of its stores.
+template <int C, typename L, typename S>
+__device__ __forceinline__ void for_groups(const RingParams& P, const Blk& B, uint32_t c, L&& load, S&& use) {
+  constexpr int E = CodecT<C>::E;
+  constexpr int U = (int)kBatch / (32 * E);
+  const int lane = lane_id();
   const uint64_t cbase = B.A + (uint64_t)c * P.chunk;
   const uint64_t lo = max(B.start, cbase);
   const uint64_t hi = min(B.start + B.len, cbase + P.chunk);
-  for (uint64_t g0 = cbase + 8ull * threadIdx.x; g0 < hi; g0 += 8ull * kRingThreads) {
-    const int vlo = (int)(max(lo, g0) - g0);
-    const int vhi = (int)(min(hi, g0 + 8) - g0);
-    fn(g0, lo, hi, vlo, vhi);
+  for (uint64_t b0 = cbase; b0 < hi; b0 += kBatch) {
+    using T = decltype(load(b0, lo, hi, 0, E));
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t g0 = b0 + (uint64_t)(u * 32 + lane) * E;
+      if (g0 < hi && g0 + E > lo) v[u] = load(g0, lo, hi, (int)(max(lo, g0) - g0), (int)(min(hi, g0 + E) - g0));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t g0 = b0 + (uint64_t)(u * 32 + lane) * E;
+      if (g0 < hi && g0 + E > lo) use(g0, lo, hi, (int)(max(lo, g0) - g0), (int)(min(hi, g0 + E) - g0), v[u]);
+    }
   }
 }
+
+template <int E>
+struct XIn {
+  FV<E> x;
+  uint4 in;
+};
 
 }  // namespace
 
 template <int C>
 __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
-  __shared__ Sh sh;
+  constexpr int E = CodecT<C>::E;
   const int G = P.G;
   const int lr = blockIdx.x / G;
-  const uint32_t j = blockIdx.x % G;
+  const uint32_t W = (uint32_t)G * kWarps;
+  const uint32_t wid = (blockIdx.x % G) * kWarps + (threadIdx.x >> 5);
   const RankCtx& R = P.rk[lr];
   const int p = P.p, r = R.rank, succ = (r + 1) % p;
   Ctl* ctl = reinterpret_cast<Ctl*>(R.inbox + P.L.off_ctl);
@@ -205,23 +244,24 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     Q8 q = q8_make(0.f);
     if constexpr (C == kQuant8) {
       uint32_t m = 0;
-      for (uint32_t c = j; c < B.nch; c += G)
-        for_groups(P, B, c, [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
-          m = max(m, absmax8_bits(load_f8(x, g0, lo, hi)));
-        });
+      for (uint32_t c = wid; c < B.nch; c += W)
+        for_groups<C>(P, B, c,
+                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                      [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
       float vmax;
-      if (!barrier_max(sh, P, R, ctl, err, 0, m, vmax, 0)) return;
+      if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
       q = q8_make(q8_scale(vmax));
     }
     uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
-    for (uint32_t c = j; c < B.nch; c += G) {
-      for_groups(P, B, c, [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-        const Packed<C> pk = encode8<C>(load_f8(x, g0, lo, hi), q, bad);
-        store_packed<C>(dst, g0 - B.A, vlo, vhi, pk);
-      });
-      publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
+    for (uint32_t c = wid; c < B.nch; c += W) {
+      for_groups<C>(P, B, c,
+                    [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                    [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
+                      store_pay<C>(dst, g0 - B.A, vlo, vhi, encode_v<C>(v, q, bad));
+                    });
+      warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) latch_error(err, kErrNonFinite, kPhRS, 0, r, r, 0);
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhRS, 0, r, r, 0);
     bad = 0;
   }
 
@@ -230,92 +270,63 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     const int b = (r - s - 1 + p) % p;
     const Blk B = get_blk(P, b);
     const bool last = (s == p - 2);
-    uint8_t* in_slot = slot_ptr(R.inbox, P.L, rs_slot(s));
+    const uint8_t* in_slot = slot_ptr(R.inbox, P.L, rs_slot(s));
     uint8_t* fwd = last ? nullptr : slot_ptr(R.peer[succ], P.L, rs_slot(s + 1));
+    auto load_xin = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
+      return XIn<E>{load_fv<E>(x, g0, lo, hi), load_pay<C>(in_slot, g0 - B.A, vlo, vhi)};
+    };
+    auto emit = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const uint4& pk, float sc) {
+      if (!last) {
+        store_pay<C>(fwd, g0 - B.A, vlo, vhi, pk);
+      } else {
+        for (int d = 1; d < p; ++d)
+          store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+        store_fv<E>(out, g0, lo, hi, decode_v<C>(pk, sc));
+      }
+    };
 
     if constexpr (C != kQuant8) {
       const Q8 q = q8_make(0.f);
-      for (uint32_t c = j; c < B.nch; c += G) {
+      for (uint32_t c = wid; c < B.nch; c += W) {
         float sin;
-        if (!await_chunk(sh, P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
-        for_groups(P, B, c, [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-          const F8 inc = decode8<C>(load_packed<C>(in_slot, g0 - B.A, vlo, vhi), sin);
-          const F8 acc = add8(load_f8(x, g0, lo, hi), inc);
-          const Packed<C> pk = encode8<C>(acc, q, bad);
-          if (!last) {
-            store_packed<C>(fwd, g0 - B.A, vlo, vhi, pk);
-          } else {
-            for (int d = 1; d < p; ++d)
-              store_packed<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
-            store_f8(out, g0, lo, hi, decode8<C>(pk, 0.f));
-          }
-        });
-        if (!last) {
-          publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
-        } else {
-          __syncthreads();
-          for (int d = 1; d < p; ++d) {
-            uint8_t* dst = R.peer[(r + d) % p];
-            if (threadIdx.x == 0) {
-              SlotHdr* h = hdr_ptr(dst, P.L, ag_slot(p, b));
-              h->seq = P.seq; h->iteration = P.iteration; h->block = (uint32_t)b;
-              h->n_elems = (uint32_t)B.len; h->scale = 0.f;
-            }
-          }
-          if (threadIdx.x == 0) {
-            fence_sys();
-            for (int d = 1; d < p; ++d)
-              st_release_sys(flag_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b), c), P.seq);
-          }
-        }
+        if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
+        for_groups<C>(P, B, c, load_xin,
+                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
+                        emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(v.x, decode_v<C>(v.in, sin)), q, bad), 0.f);
+                      });
+        if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
+        else warp_publish_all(P, R, b, c, B.len, 0.f);
       }
     } else {
       // pass A: fold into `out` (scratch for this block) and reduce the max
       uint32_t m = 0;
-      for (uint32_t c = j; c < B.nch; c += G) {
+      for (uint32_t c = wid; c < B.nch; c += W) {
         float sin;
-        if (!await_chunk(sh, P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
-        for_groups(P, B, c, [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-          const F8 inc = decode8<C>(load_packed<C>(in_slot, g0 - B.A, vlo, vhi), sin);
-          const F8 acc = add8(load_f8(x, g0, lo, hi), inc);
-          m = max(m, absmax8_bits(acc));
-          store_f8(out, g0, lo, hi, acc);
-        });
+        if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
+        for_groups<C>(P, B, c, load_xin,
+                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
+                        const FV<E> acc = add_v(v.x, decode_v<C>(v.in, sin));
+                        m = max(m, absmax_bits(acc));
+                        store_fv<E>(out, g0, lo, hi, acc);
+                      });
       }
       float vmax;
-      if (!barrier_max(sh, P, R, ctl, err, s + 1, m, vmax, s)) return;
+      if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
       const Q8 q = q8_make(q8_scale(vmax));
       // pass B: encode the partial with the block scale and push it
-      for (uint32_t c = j; c < B.nch; c += G) {
-        for_groups(P, B, c, [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-          const F8 acc = load_f8_cg(out, g0, lo, hi);
-          const Packed<C> pk = encode8<C>(acc, q, bad);
-          if (!last) {
-            store_packed<C>(fwd, g0 - B.A, vlo, vhi, pk);
-          } else {
-            for (int d = 1; d < p; ++d)
-              store_packed<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
-            store_f8(out, g0, lo, hi, decode8<C>(pk, q.s));
-          }
-        });
-        if (!last) {
-          publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
-        } else {
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            for (int d = 1; d < p; ++d) {
-              SlotHdr* h = hdr_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b));
-              h->seq = P.seq; h->iteration = P.iteration; h->block = (uint32_t)b;
-              h->n_elems = (uint32_t)B.len; h->scale = q.s;
-            }
-            fence_sys();
-            for (int d = 1; d < p; ++d)
-              st_release_sys(flag_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b), c), P.seq);
-          }
-        }
+      for (uint32_t c = wid; c < B.nch; c += W) {
+        for_groups<C>(P, B, c,
+                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
+                        return load_fv<E, false>(out, g0, lo, hi);
+                      },
+                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const FV<E>& acc) {
+                        emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
+                      });
+        if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
+        else warp_publish_all(P, R, b, c, B.len, q.s);
       }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0)
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
       latch_error(err, kErrNonFinite, last ? kPhAG : kPhRS, last ? 0 : s + 1, b, r, 0);
     bad = 0;
   }
@@ -325,13 +336,17 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     const int b = (r + 1 + k) % p;  // own block is (r+1)%p
     const Blk B = get_blk(P, b);
     const int step = (r - b + p) % p;  // reference allgather step that delivers block b
-    uint8_t* in_slot = slot_ptr(R.inbox, P.L, ag_slot(p, b));
-    for (uint32_t c = j; c < B.nch; c += G) {
+    const uint8_t* in_slot = slot_ptr(R.inbox, P.L, ag_slot(p, b));
+    for (uint32_t c = wid; c < B.nch; c += W) {
       float sin;
-      if (!await_chunk(sh, P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) return;
-      for_groups(P, B, c, [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-        store_f8(out, g0, lo, hi, decode8<C>(load_packed<C>(in_slot, g0 - B.A, vlo, vhi), sin));
-      });
+      if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) return;
+      for_groups<C>(P, B, c,
+                    [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
+                      return load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
+                    },
+                    [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const uint4& v) {
+                      store_fv<E>(out, g0, lo, hi, decode_v<C>(v, sin));
+                    });
     }
   }
 }
@@ -344,5 +359,7 @@ void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError
                                          : (const void*)ring_allreduce_kernel<kQuant8>;
   *err = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, stream);
 }
+
+int ring_warps_per_cta() { return kWarps; }
 
 }  // namespace gp

@@ -7,8 +7,9 @@
 namespace gp {
 
 constexpr int kRingThreads = 512;
-constexpr uint32_t kMinChunk = 1024;   // elements; flags are sized for this
-constexpr uint32_t kMaxChunk = 16384;  // elements per chunk (64 KiB of fp32)
+constexpr int kRingWarps = kRingThreads / 32;
+constexpr uint32_t kMinChunk = 1024;   // elements per warp chunk; flags are sized for this
+constexpr uint32_t kMaxChunk = 4096;   // default largest warp chunk (16 KiB of fp32)
 
 // Per-rank inbox layout (identical on every rank of a communicator). Peers
 // write payload, headers and flags here over NVLink; ctl/err are private.
@@ -48,7 +49,7 @@ struct RingParams {
   uint64_t timeout_ns;
   uint32_t seq, iteration;
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
-  int p, codec, G;             // world size, codec tag, CTAs per rank
+  int p, codec, G;             // world size, codec tag, CTAs per rank (16 warp workers each)
 };
 
 __host__ __device__ inline int rs_slot(int s) { return s; }

@@ -1,0 +1,446 @@
+"""Pipe-SGD training engine on B200: width-K pipeline on two CUDA streams.
+
+Drop-in for the train-step path of /root/reference/pkg/src/gradpipe/engine.py:
+`RunConfig` (:80-107), `WorkerResult` (:110-120), `aggregate_mean` (:123-129),
+`effective_mode` (:132-136), `GradientBuffer` (:188-235), `run_inproc_cluster`
+(:563-618), plus `run_process_worker` (one rank per process under torchrun,
+the analogue of `run_tcp_worker`, :621-646).
+
+Reference structure -> B200 structure
+  compute thread (:418-431)        -> compute stream: consume(t-K) -> fwd/bwd(t)
+                                      -> local pre-compress D(C(grad_t))
+  comm thread (:392-412)           -> comm stream: fused ring(t) -> whole-vector
+                                      re-compress of the sum into slot t (:407)
+  _LocalGradientMailbox (:139-185) -> K device buffers + "local ready" events
+  GradientBuffer slots (:188-235)  -> K compressed device slots + "aggregated
+                                      ready" events; write-once/take-clears
+                                      bookkeeping kept on the host
+  _apply_update (:302-307)         -> gp_consume_update: decode slot, fl(g/p),
+                                      fl(w - fl(lr*g)) in one HBM pass
+One host thread per rank only *enqueues*; the two streams overlap iteration
+t's allreduce with iteration t+1's update + forward/backward exactly as in
+Alg. 1 (update at t consumes the aggregated gradient of t-K; slots for
+tags t_start-K..t_start-1 are zero; K in-flight gradients are drained).
+d_sync is the same machinery with depth 1, no re-compress and the compute
+stream waiting for the ring every iteration (engine.py:340-375).
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .collective import allreduce_into
+from .compression import Codec, CodecStatus, as_codec, encode_async, roundtrip_async
+from .errors import CodecError, ConfigError, EngineError
+from .models import FlatModel, ModelSpec, SpecNet, init_params
+from .transport import EmulatedTransport, GpuEndpoint, GpuTransport, TrafficStats
+
+MODE_PS_SYNC = "ps_sync"
+MODE_D_SYNC = "d_sync"
+MODE_PIPE_SGD = "pipe_sgd"
+MODES = (MODE_PS_SYNC, MODE_D_SYNC, MODE_PIPE_SGD)
+
+STAGE_UPDATE = "update"
+STAGE_FORWARD = "forward"
+STAGE_BACKWARD = "backward"
+STAGE_COMPRESS = "compress"
+STAGE_ALLREDUCE = "allreduce"
+STAGE_DECOMPRESS = "decompress"
+STAGE_BARRIER = "barrier"
+STAGE_IDLE = "idle"
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    rank: int
+    iteration: int
+    stage: str
+    start_ns: int
+    end_ns: int
+    consumed_tag: int | None = None
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    mode: str = MODE_D_SYNC
+    iterations: int = 100
+    learning_rate: float = 0.05
+    codec: Codec = Codec.NONE
+    depth: int = 2  # iteration dependency K (pipe_sgd only)
+    batch_size: int = 32
+    warmup_epochs: int = 0
+    eval_interval: int = 0
+    seed: int = 0
+    lr_decay_every: int = 0
+    lr_decay_factor: float = 1.0
+    snapshot_first: int = 0
+
+    def __post_init__(self) -> None:
+        if self.mode not in MODES:
+            raise ConfigError(f"unknown mode {self.mode!r}")
+        if self.mode == MODE_PS_SYNC:
+            raise ConfigError("ps_sync (parameter server) is not on the GPU hot path; use d_sync or pipe_sgd")
+        if self.iterations < 1:
+            raise ConfigError("need at least one iteration")
+        if self.learning_rate <= 0:
+            raise ConfigError("learning rate must be positive")
+        if self.mode == MODE_PIPE_SGD and self.depth < 2:
+            raise ConfigError("pipelined training needs depth K >= 2")
+        if self.batch_size < 1:
+            raise ConfigError("batch size must be >= 1")
+        if self.warmup_epochs < 0 or self.eval_interval < 0:
+            raise ConfigError("warmup_epochs and eval_interval must be >= 0")
+        object.__setattr__(self, "codec", as_codec(self.codec))
+
+
+@dataclass
+class WorkerResult:
+    rank: int
+    params: np.ndarray
+    trace: list[TraceEvent]
+    metrics: list[tuple[int, float, float]]  # (iteration, wall_ms, train_loss)
+    eval_points: list[tuple[int, np.ndarray]]
+    early_params: list[tuple[int, np.ndarray]]
+    stats: TrafficStats
+    train_seconds: float
+    is_server: bool = False
+    device_seconds: float = 0.0
+
+
+def aggregate_mean(total, p: int):
+    """Aggregated gradient sum -> mean over the global batch (fp32 division)."""
+    if p < 1:
+        raise ConfigError("worker count must be >= 1")
+    if p == 1:
+        return total
+    if isinstance(total, torch.Tensor):
+        return total / torch.tensor(p, dtype=torch.float32, device=total.device)
+    return (np.asarray(total, np.float32) / np.float32(p)).astype(np.float32)
+
+
+def effective_mode(config: RunConfig, epoch: int) -> str:
+    if config.mode != MODE_PIPE_SGD:
+        return config.mode
+    return MODE_D_SYNC if epoch < config.warmup_epochs else MODE_PIPE_SGD
+
+
+class GradientBuffer:
+    """Depth-K ring of aggregated-gradient slots (engine.py:188-235).
+
+    Host-side bookkeeping with the reference's contract: the slot for tag t
+    is written once, `take` clears it, a second write to an occupied slot is
+    an EngineError. Each slot carries the CUDA event that marks its device
+    data ready, so `take` never blocks the host: the consumer's stream waits."""
+
+    def __init__(self, depth: int, timeout_s: float = 30.0):
+        self.depth = depth
+        self._slots: list = [None] * depth
+        self._lock = threading.Lock()
+
+    def put(self, tag: int, block, ready: torch.cuda.Event | None = None) -> None:
+        idx = tag % self.depth
+        with self._lock:
+            if self._slots[idx] is not None:
+                raise EngineError(f"aggregated-gradient slot for iteration {tag} written twice "
+                                  f"(still holds iteration {self._slots[idx][0]})")
+            self._slots[idx] = (tag, block, ready)
+
+    def take(self, tag: int, stream: torch.cuda.Stream | None = None):
+        idx = tag % self.depth
+        with self._lock:
+            if self._slots[idx] is None:
+                raise EngineError(f"aggregated gradient {tag} was never produced")
+            slot_tag, block, ready = self._slots[idx]
+            if slot_tag != tag:
+                raise EngineError(f"slot {idx} holds iteration {slot_tag}, expected {tag}")
+            self._slots[idx] = None
+        if ready is not None and stream is not None:
+            stream.wait_event(ready)
+        return block
+
+
+@dataclass
+class _Slot:
+    """A compressed aggregated gradient on the device."""
+    codec: Codec
+    payload: torch.Tensor      # uint8, n * width bytes
+    status: CodecStatus        # quant8 scale at status.scale_view
+
+
+BatchFn = Callable[[int, int], tuple]
+
+
+class RankEngine:
+    """One rank's Pipe-SGD loop on one GPU (enqueue-only host thread)."""
+
+    def __init__(self, rank: int, world: int, endpoint: GpuEndpoint, fm: FlatModel, config: RunConfig,
+                 batch_fn: BatchFn, trace: bool = True, grad_fn=None):
+        self.rank, self.world, self.ep, self.fm, self.cfg = rank, world, endpoint, fm, config
+        self.batch_fn = batch_fn
+        self.grad_fn = grad_fn
+        self.dev = fm.params.device
+        self.n = fm.num_params
+        self.cs = torch.cuda.Stream(self.dev)
+        self.ms = torch.cuda.Stream(self.dev)
+        self.tracing = trace
+        self.events: list = []  # (iteration, stage, ev0, ev1, consumed)
+        K = max(config.depth, 1)
+        self.K = K
+        w = config.codec.bytes_per_elem
+        with torch.cuda.device(self.dev):
+            self.local = [torch.empty(self.n, dtype=torch.float32, device=self.dev) for _ in range(K)]
+            self.summed = torch.empty(self.n, dtype=torch.float32, device=self.dev)
+            self.slots = [_Slot(config.codec, torch.zeros(self.n * w, dtype=torch.uint8, device=self.dev),
+                                CodecStatus(self.dev)) for _ in range(K)]
+            self.sync_slot = _Slot(Codec.NONE, self.summed.view(torch.uint8), CodecStatus(self.dev))
+            self.local_status = [CodecStatus(self.dev) for _ in range(K)]
+            self.slot_nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self.losses = torch.zeros(config.iterations + 1, dtype=torch.float32, device=self.dev)
+        self.ev_local = [torch.cuda.Event() for _ in range(K)]
+        self.buffer = GradientBuffer(K)
+        self.iter_done: dict[int, torch.cuda.Event] = {}
+        self.early_params: list = []
+        self.eval_points: list = []
+        self.updates_seen = 0
+
+    # ---------------------------------------------------------------- helpers
+    def _lr(self, t: int) -> float:
+        c = self.cfg
+        if c.lr_decay_every <= 0:
+            return c.learning_rate
+        return c.learning_rate * (c.lr_decay_factor ** ((t - 1) // c.lr_decay_every))
+
+    def _ev(self, stream):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def _rec(self, t, stage, e0, e1, consumed=None):
+        if self.tracing:
+            self.events.append((t, stage, e0, e1, consumed))
+
+    def _consume(self, slot: _Slot, tag: int, t: int) -> None:
+        """w <- fl(w - fl(lr * fl(D(slot) / p)))   on the compute stream."""
+        lr = float(np.float32(self._lr(t)))
+        e0 = self._ev(self.cs) if self.tracing else None
+        _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
+                  slot.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+        if self.tracing:
+            self._rec(t, STAGE_UPDATE, e0, self._ev(self.cs), tag)
+        self.updates_seen += 1
+        if self.updates_seen <= self.cfg.snapshot_first:
+            self.early_params.append((t, self.fm.params.clone()))
+
+    def _compute_local(self, t: int) -> None:
+        """fwd + bwd + whole-vector D(C(grad)) into local[t % K] (engine.py:323-336)."""
+        i = t % self.K
+        e0 = self._ev(self.cs) if self.tracing else None
+        if self.grad_fn is not None:
+            self.cs.synchronize()
+            loss, g = self.grad_fn(self.rank, t, self.fm.params)
+            self.fm.grads.copy_(torch.as_tensor(np.asarray(g, np.float32)).to(self.dev))
+            self.losses[t].fill_(float(loss))
+        else:
+            x, y = self.batch_fn(self.rank, t)
+            loss = self.fm.loss_and_grad(x, y)
+            self.losses[t].copy_(loss)
+        e1 = self._ev(self.cs) if self.tracing else None
+        roundtrip_async(self.fm.grads, self.cfg.codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+        self.ev_local[i].record(self.cs)
+        if self.tracing:
+            self._rec(t, STAGE_BACKWARD, e0, e1)
+            self._rec(t, STAGE_COMPRESS, e1, self._ev(self.cs))
+        if self.cfg.eval_interval and self.rank == 0 and t % self.cfg.eval_interval == 0:
+            self.eval_points.append((t, self.fm.params.clone()))
+
+    def _communicate(self, t: int, requant: bool) -> _Slot:
+        """Comm stream: ring(local[t]) -> (pipe) C(sum) into slot t."""
+        i = t % self.K
+        self.ms.wait_event(self.ev_local[i])
+        e0 = self._ev(self.ms) if self.tracing else None
+        allreduce_into(self.local[i], self.summed, self.ep, self.cfg.codec, t, self.ms)
+        if requant:
+            slot = self.slots[i]
+            encode_async(self.summed, self.cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
+        else:
+            slot = self.sync_slot
+        ready = torch.cuda.Event(enable_timing=self.tracing)
+        ready.record(self.ms)
+        if self.tracing:
+            self._rec(t, STAGE_ALLREDUCE, e0, ready)
+        self.buffer.put(t, slot, ready)
+        return slot
+
+    # ------------------------------------------------------------------ loops
+    def sync_phase(self, t0: int, t1: int) -> None:
+        """d_sync (engine.py:340-375): update(pending) -> compute -> ring."""
+        pending = None
+        for t in range(t0, t1 + 1):
+            if pending is not None:
+                self._consume(self.buffer.take(pending, self.cs), pending, t)
+            self._compute_local(t)
+            self._communicate(t, requant=False)
+            pending = t
+            self._mark(t)
+        if pending is not None:
+            self._consume(self.buffer.take(pending, self.cs), pending, pending + 1)
+
+    def pipe_phase(self, t0: int, t1: int) -> None:
+        """pipe_sgd (engine.py:379-448) with zero-primed slots and K-drain."""
+        K = self.K
+        for tag in range(t0 - K, t0):
+            slot = self.slots[tag % K]
+            slot.payload.zero_()
+            slot.status.t.zero_()
+            ev = torch.cuda.Event()
+            ev.record(self.cs)
+            self.buffer.put(tag, slot, ev)
+        for t in range(t0, t1 + 1):
+            self._consume(self.buffer.take(t - K, self.cs), t - K, t)
+            self._compute_local(t)
+            self._communicate(t, requant=True)
+            self._mark(t)
+        for tag in range(t1 - K + 1, t1 + 1):
+            self._consume(self.buffer.take(tag, self.cs), tag, tag + K)
+
+    def _mark(self, t):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self.cs)
+        self.iter_done[t] = e
+
+    def run(self, iters_per_epoch: int = 1) -> None:
+        cfg = self.cfg
+        # every torch op issued below (batch gather, fwd/bwd, snapshots) goes
+        # to the compute stream; ring + re-compress are put on self.ms explicitly
+        with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
+            if cfg.mode == MODE_D_SYNC:
+                self.sync_phase(1, cfg.iterations)
+            else:
+                warm = min(cfg.iterations, cfg.warmup_epochs * iters_per_epoch)
+                if warm > 0:
+                    self.sync_phase(1, warm)
+                if warm < cfg.iterations:
+                    self.pipe_phase(warm + 1, cfg.iterations)
+            self.end = torch.cuda.Event(enable_timing=True)
+            self.end.record(self.cs)
+
+    def finish(self, start_ev: torch.cuda.Event, train_seconds: float) -> WorkerResult:
+        self.cs.synchronize()
+        self.ms.synchronize()
+        self.ep._check_errors(self.n)
+        if any(int(s.t[1].item()) for s in self.local_status):
+            raise CodecError("refusing to compress non-finite values")
+        losses = self.losses.cpu().numpy()
+        metrics = [(t, start_ev.elapsed_time(e), float(losses[t])) for t, e in sorted(self.iter_done.items())]
+        trace = []
+        for t, stage, e0, e1, consumed in self.events:
+            trace.append(TraceEvent(self.rank, t, stage, int(start_ev.elapsed_time(e0) * 1e6),
+                                    int(start_ev.elapsed_time(e1) * 1e6), consumed))
+        trace.sort(key=lambda e: (e.start_ns, e.iteration))
+        dev_s = start_ev.elapsed_time(self.end) / 1e3
+        return WorkerResult(
+            rank=self.rank, params=self.fm.params.cpu().numpy(), trace=trace, metrics=metrics,
+            eval_points=[(t, p.cpu().numpy()) for t, p in self.eval_points],
+            early_params=[(t, p.cpu().numpy()) for t, p in self.early_params],
+            stats=self.ep.stats.snapshot(), train_seconds=train_seconds, device_seconds=dev_s)
+
+
+# ----------------------------------------------------------------- clusters
+
+def _make_transport(workers: int, timeout_s: float, max_elems: int):
+    if torch.cuda.device_count() >= workers:
+        return GpuTransport(workers, timeout_s=timeout_s, max_elems=max_elems)
+    return EmulatedTransport(workers, timeout_s=timeout_s, max_elems=max_elems)
+
+
+class DeviceDataset:
+    """Per-device copy of a (features, labels) dataset with reference-exact
+    host-side batch sampling (data.py:41-43 shard, :57-63 sample_from_shard)."""
+
+    def __init__(self, dataset, device):
+        self.features = torch.as_tensor(np.asarray(dataset.features, np.float32)).to(device)
+        self.labels = torch.as_tensor(np.asarray(dataset.labels, np.int64)).to(device)
+        self.num_samples = int(self.features.shape[0])
+        self.device = device
+
+    def gather(self, idx: np.ndarray):
+        it = torch.as_tensor(np.asarray(idx, np.int64)).to(self.device, non_blocking=False)
+        return self.features.index_select(0, it), self.labels.index_select(0, it)
+
+
+def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_s: float = 0.0,
+                       byte_time_s: float = 0.0, batch_provider=None, timeout_s: float = 30.0,
+                       transport=None, grad_fn=None, trace: bool = True) -> list[WorkerResult]:
+    """Run a full training job with all ranks as threads of this process
+    (engine.py:563-618), one GPU per rank (GpuTransport) or all ranks on one
+    GPU (EmulatedTransport) when there are fewer GPUs than workers.
+
+    `model` is a ModelSpec (logistic / MLP, reference layout and init);
+    `grad_fn(rank, t, params) -> (loss, grad)` optionally replaces the model's
+    forward/backward (used by parity tests to inject oracle gradients)."""
+    if workers < 1:
+        raise ConfigError("need at least one worker")
+    if latency_s or byte_time_s:
+        raise ConfigError("GPU transports do not inject synthetic delays")
+    if not isinstance(model, ModelSpec):
+        model = ModelSpec(model.kind, tuple(model.layer_dims))
+    n = model.num_params
+    own_transport = transport is None
+    tr = transport or _make_transport(workers, timeout_s, max(n, 1))
+    shards = [np.arange(r % workers, dataset.features.shape[0], workers) for r in range(workers)]
+    if batch_provider is None and grad_fn is None:
+        for r in range(workers):
+            if config.batch_size > len(shards[r]):
+                raise ConfigError(f"rank {r}: batch size {config.batch_size} exceeds shard of "
+                                  f"{len(shards[r])} samples")
+    results: list = [None] * workers
+    errors: list = []
+    barrier = threading.Barrier(workers)
+
+    def runner(r: int):
+        try:
+            ep = tr.endpoint(r)
+            dev = ep.device
+            with torch.cuda.device(dev):
+                fm = FlatModel(SpecNet(model), dev, init_params(model, config.seed))
+                data = DeviceDataset(dataset, dev) if grad_fn is None else None
+                rng = np.random.default_rng([config.seed, r])
+
+                def batch_fn(rank, t):
+                    idx = batch_provider(rank, t) if batch_provider else \
+                        shards[rank][rng.choice(len(shards[rank]), size=config.batch_size, replace=False)]
+                    return data.gather(idx)
+
+                eng = RankEngine(r, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn)
+                ipe = max(1, len(shards[r]) // config.batch_size)
+                torch.cuda.synchronize(dev)
+                barrier.wait()
+                start = torch.cuda.Event(enable_timing=True)
+                start.record(eng.cs)
+                eng.ms.wait_stream(eng.cs)
+                t0 = time.perf_counter()
+                eng.run(ipe)
+                eng.cs.synchronize()
+                results[r] = eng.finish(start, time.perf_counter() - t0)
+        except BaseException as err:  # noqa: BLE001
+            errors.append(err)
+            barrier.abort()
+
+    threads = [threading.Thread(target=runner, args=(r,), name=f"worker-{r}") for r in range(workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if own_transport:
+        tr.close()
+    if errors:
+        real = [e for e in errors if not isinstance(e, threading.BrokenBarrierError)]
+        raise (real or errors)[0]
+    return results

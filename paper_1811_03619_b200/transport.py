@@ -97,17 +97,25 @@ class GpuEndpoint:
 
     recv = send
 
+    def info(self) -> dict:
+        """Communicator facts: CTAs per rank, inbox bytes, calls issued."""
+        o = (ctypes.c_int64 * 8)()
+        _lib.call("gp_comm_info", self._comm, o)
+        keys = ("rank", "world", "device", "max_elems", "ctas", "inbox_bytes", "seq", "emulated")
+        return dict(zip(keys, [int(v) for v in o]))
+
     # -- internals --------------------------------------------------------
     def _raw_stats(self) -> TrafficStats:
         s = _lib.GpStats()
         _lib.call("gp_get_stats", self._comm, self.rank, ctypes.byref(s))
         return TrafficStats(int(s.messages), int(s.payload_bytes), int(s.frame_bytes))
 
-    def _launch(self, x: torch.Tensor, out: torch.Tensor, codec: int, iteration: int, stream: int) -> None:
+    def _launch(self, x: torch.Tensor, out: torch.Tensor, codec: int, iteration: int,
+                stream: torch.cuda.Stream) -> None:
         if self._poisoned:
             raise CollectiveError(f"endpoint {self.rank} is unusable after an earlier failure: {self._poisoned}")
         _lib.call("gp_allreduce", self._comm, x.data_ptr(), out.data_ptr(), x.numel(), int(codec),
-                  int(iteration) & 0xFFFFFFFF, stream)
+                  int(iteration) & 0xFFFFFFFF, stream.cuda_stream)
 
     def _check_errors(self, n: int) -> None:
         """After the launching stream completed: raise what the device latched."""
@@ -182,41 +190,35 @@ class GpuTransport:
         self._comms = []
 
 
-class _Rendezvous:
-    """Collects one call per virtual rank, launches the emulated ring once."""
-
-    def __init__(self, p: int, timeout_s: float):
-        self.p = p
-        self.timeout_s = timeout_s
-        self.cv = threading.Condition()
+class _Generation:
+    def __init__(self):
         self.slots: dict[int, tuple] = {}
-        self.generation = 0
-        self.done_gen = -1
+        self.done: torch.cuda.Event | None = None
+        self.n = 0
         self.error: Exception | None = None
+        self.polled = False
+        self.launched = False
 
 
 class EmulatedEndpoint(GpuEndpoint):
-    def _launch(self, x, out, codec, iteration, stream):  # rendezvous instead of a lone launch
-        tr: EmulatedTransport = self._transport
-        tr._arrive(self.rank, x, out, codec, iteration)
+    """Endpoint of an EmulatedTransport: its calls rendezvous with the other
+    virtual ranks; the last arrival launches the ring for everyone."""
+
+    def _launch(self, x, out, codec, iteration, stream):
+        self._gen = self._transport._arrive(self.rank, x, out, codec, iteration, stream)
 
     def _check_errors(self, n: int) -> None:
-        tr: EmulatedTransport = self._transport
-        tr._finish(self.rank)
-
-    def _raw_stats(self) -> TrafficStats:
-        s = _lib.GpStats()
-        _lib.call("gp_get_stats", self._comm, self.rank, ctypes.byref(s))
-        return TrafficStats(int(s.messages), int(s.payload_bytes), int(s.frame_bytes))
+        self._transport._finish(getattr(self, "_gen", None))
 
 
 class EmulatedTransport:
     """p ranks of the ring on one GPU, one cooperative launch per allreduce.
 
-    Ranks may call from p threads exactly like InProcTransport endpoints; the
-    last arrival launches `gp_allreduce_emulated` for everyone. Used to check
-    ring parity at p = 3/4/8 on a single B200 without separately launched
-    kernels that wait on each other."""
+    Ranks call from p threads exactly like InProcTransport endpoints. Every
+    call is stream-ordered: the launch waits on each rank's stream (event) and
+    each rank's stream waits on the launch, so callers never block on the GPU
+    unless they ask to (ring_allreduce does). Used for parity at p = 3/4/8 on
+    a single B200 without separately launched kernels that wait on each other."""
 
     def __init__(self, world_size: int, latency_s: float = 0.0, byte_time_s: float = 0.0,
                  timeout_s: float = DEFAULT_TIMEOUT_S, device: int = 0,
@@ -230,7 +232,9 @@ class EmulatedTransport:
         _lib.call("gp_comm_create_emulated", world_size, device, max_elems, ctypes.byref(h))
         self._comm = h
         _lib.call("gp_comm_set_tuning", h, int(ctas), float(timeout_s))
-        self._rv = _Rendezvous(world_size, timeout_s)
+        self._cv = threading.Condition()
+        self._cur = _Generation()
+        self._poll_lock = threading.Lock()
         self._eps = [EmulatedEndpoint(r, world_size, self.device, h, timeout_s, transport=self)
                      for r in range(world_size)]
         self._stream = torch.cuda.Stream(self.device)
@@ -238,58 +242,67 @@ class EmulatedTransport:
     def endpoint(self, rank: int) -> EmulatedEndpoint:
         return self._eps[rank]
 
-    def _arrive(self, rank, x, out, codec, iteration):
-        rv = self._rv
-        with rv.cv:
-            gen = rv.generation
-            if rank in rv.slots:
+    def _arrive(self, rank, x, out, codec, iteration, stream) -> _Generation:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        with self._cv:
+            gen = self._cur
+            if rank in gen.slots:
                 raise CollectiveError(f"rank {rank} entered the same allreduce twice")
-            rv.slots[rank] = (x, out, int(codec), int(iteration), x.numel())
-            if len(rv.slots) == rv.p:
-                self._launch_all()
-                rv.generation += 1
-                rv.cv.notify_all()
+            gen.slots[rank] = (x, out, int(codec), int(iteration), x.numel(), ev)
+            if len(gen.slots) == self.world_size:
+                self._launch_all(gen)
+                self._cur = _Generation()
+                self._cv.notify_all()
             else:
-                ok = rv.cv.wait_for(lambda: rv.generation != gen, timeout=rv.timeout_s)
+                ok = self._cv.wait_for(lambda: gen.launched, timeout=self.timeout_s)
                 if not ok:
-                    rv.slots.pop(rank, None)
-                    raise CollectiveError(f"reduce-scatter step 0 (rank {rank} <- {(rank - 1) % rv.p}): "
-                                          f"timed out after {rv.timeout_s:g}s")
+                    gen.slots.pop(rank, None)
+                    raise CollectiveError(f"reduce-scatter step 0 (rank {rank} <- {(rank - 1) % self.world_size}): "
+                                          f"timed out after {self.timeout_s:g}s")
+        if gen.error is None and gen.done is not None:
+            stream.wait_event(gen.done)
+        return gen
 
-    def _launch_all(self):
-        rv = self._rv
-        args = [rv.slots[r] for r in range(rv.p)]
-        rv.slots = {}
-        ns = {a[4] for a in args}
-        codecs = {a[2] for a in args}
-        its = {a[3] for a in args}
-        rv.error = None
-        if len(ns) != 1 or len(codecs) != 1 or len(its) != 1:
-            rv.error = CollectiveError("reduce-scatter step 0: ranks disagree on vector length, codec or "
-                                       "iteration (unequal vector lengths across ranks?)")
+    def _launch_all(self, gen: _Generation):
+        p = self.world_size
+        args = [gen.slots[r] for r in range(p)]
+        gen.launched = True
+        if len({a[4] for a in args}) != 1 or len({a[2] for a in args}) != 1 or len({a[3] for a in args}) != 1:
+            gen.error = CollectiveError("reduce-scatter step 0: ranks disagree on vector length, codec or "
+                                        "iteration (unequal vector lengths across ranks?)")
             return
-        n = ns.pop()
-        ins = (ctypes.c_void_p * rv.p)(*[a[0].data_ptr() for a in args])
-        outs = (ctypes.c_void_p * rv.p)(*[a[1].data_ptr() for a in args])
-        cur = torch.cuda.current_stream(self.device)
-        self._stream.wait_stream(cur)
+        gen.n = args[0][4]
+        ins = (ctypes.c_void_p * p)(*[a[0].data_ptr() for a in args])
+        outs = (ctypes.c_void_p * p)(*[a[1].data_ptr() for a in args])
         for a in args:
+            self._stream.wait_event(a[5])
             a[0].record_stream(self._stream)
             a[1].record_stream(self._stream)
-        _lib.call("gp_allreduce_emulated", self._comm, ins, outs, n, codecs.pop(), its.pop() & 0xFFFFFFFF,
+        _lib.call("gp_allreduce_emulated", self._comm, ins, outs, gen.n, args[0][2], args[0][3] & 0xFFFFFFFF,
                   self._stream.cuda_stream)
-        self._stream.synchronize()
-        e = _lib.GpError()
-        _lib.call("gp_comm_poll_error", self._comm, ctypes.byref(e))
-        if e.kind:
-            rv.error = raise_for(e, rv.p, n, rv.timeout_s)
+        gen.done = torch.cuda.Event()
+        gen.done.record(self._stream)
+        gen.slots = {}
 
-    def _finish(self, rank):
-        if self._rv.error is not None:
-            raise self._rv.error
+    def _finish(self, gen: _Generation | None):
+        if gen is None:
+            return
+        if gen.error is None and not gen.polled:
+            gen.done.synchronize()
+            with self._poll_lock:
+                if not gen.polled:
+                    e = _lib.GpError()
+                    _lib.call("gp_comm_poll_error", self._comm, ctypes.byref(e))
+                    if e.kind:
+                        gen.error = raise_for(e, self.world_size, gen.n, self.timeout_s)
+                    gen.polled = True
+        if gen.error is not None:
+            raise gen.error
 
     def close(self) -> None:
         if self._comm:
+            torch.cuda.synchronize(self.device)
             _lib.load().gp_comm_destroy(self._comm)
             self._comm = None
 
