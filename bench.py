@@ -1,0 +1,473 @@
+"""Pipe-SGD benchmark: width-2 Pipe-SGD iterations/s with the fused compressed
+ring AllReduce on B200, plus ring bus bandwidth, roofline and CPU baselines.
+
+    python bench.py [--gpus 1] [--steps 30] [--warmup 5]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
+        --master-port P bench.py --gpus N --steps K --warmup W
+    python bench.py --impl reference ...     # the reference's CPU path (oracle port)
+
+Workload (BASELINE.json configs[1], "C2"): CIFAR-10-shaped small CNN
+(4,710,538 fp32 params), Pipe-SGD width 2, trunc16 ring compression, fixed
+global batch split over N GPUs (strong scaling, as in the paper's setup).
+One step = one Pipe-SGD iteration on every rank: consume the aggregated
+gradient of t-2 (decode, /p, SGD), forward+backward on the rank's batch,
+whole-vector D(C(grad)), fused compressed ring AllReduce on the comm stream,
+whole-vector re-compress of the sum into slot t. Prints ONE JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Pipe-SGD iters/sec & compressed ring-allreduce bus GB/s at 1/2/4/8 B200"
+NVLINK_PEAK_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction (MEASURED_PEAKS has no NVLink)
+L2_BYTES = 126.5 * 2**20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="c2")
+    ap.add_argument("--codec", default="trunc16")
+    ap.add_argument("--mode", default="pipe_sgd")
+    ap.add_argument("--depth", type=int, default=2)
+    ap.add_argument("--global-batch", type=int, default=512)
+    ap.add_argument("--ctas", type=int, default=32,
+                    help="CTAs the ring kernel may occupy per GPU (the rest keep computing)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-allreduce-sweep", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_model():
+    try:
+        return [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:  # noqa: BLE001
+        return "unknown"
+
+
+# ------------------------------------------------- the reference's CPU path
+
+def oracle_iteration(grads, w, codec, p, lr, state):
+    """One Pipe-SGD iteration of the reference's hot path, restated by the
+    oracle (engine.py:333/:355 local D(C(g)), collective.py ring, engine.py:407
+    re-compress, :420-426 decompress, :123-129 mean, models.py:198-204 SGD).
+    Consumes the slot of t-2, produces slot t (width 2)."""
+    from oracle import codec as OC
+    from oracle import engine as OE
+    from oracle import ring as OR
+    local = [OC.roundtrip(g, codec) for g in grads]
+    summed = OR.ring_allreduce_all(local, codec).outputs[0] if p > 1 else local[0].copy()
+    state.append(OC.encode(summed, codec))
+    slot = state.pop(0)
+    agg = OC.decode(codec, *slot)
+    return OE.sgd_update(w, OE.aggregate_mean(agg, p), lr)
+
+
+class CpuPath:
+    """The reference path on this host's CPU for an n-element gradient and p
+    simulated ranks (one thread, numpy, inputs generated once)."""
+
+    def __init__(self, n, p, codec):
+        from oracle import codec as OC
+        g = np.random.default_rng(0)
+        self.grads = [(g.normal(0, 1e-2, n)).astype(np.float32) for _ in range(p)]
+        self.w = g.normal(0, 0.05, n).astype(np.float32)
+        zero = OC.encode(np.zeros(n, np.float32), codec)
+        self.state = [zero, zero]
+        self.p, self.codec = p, codec
+
+    def step(self):
+        self.w = oracle_iteration(self.grads, self.w, self.codec, self.p, 0.05, self.state)
+
+
+def cpu_path_rate(n, p, codec, seconds, max_iters=1000):
+    """Iterations/s of the reference path on this host, bounded to `seconds`."""
+    cp = CpuPath(n, p, codec)
+    cp.step()  # warm
+    t0 = time.perf_counter()
+    k = 0
+    while k < max_iters and (k < 2 or time.perf_counter() - t0 < seconds):
+        cp.step()
+        k += 1
+    dt = time.perf_counter() - t0
+    return k / dt, k, dt
+
+
+def reference_arm(args, ws, rank):
+    if rank != 0:
+        return None
+    from oracle import codec as OC
+    from paper_1811_03619_b200.models import build_torch_model
+    mod, _, _ = build_torch_model(args.model)
+    n = sum(p.numel() for p in mod.parameters())
+    codec = {"none": OC.NONE, "trunc16": OC.TRUNC16, "quant8": OC.QUANT8}[args.codec]
+    p = max(1, args.gpus)
+    cp = CpuPath(n, p, codec)
+    for _ in range(args.warmup):
+        cp.step()
+    per_step = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cp.step()
+        per_step.append(time.perf_counter() - t0)
+    t = float(np.mean(per_step))
+    v = 1.0 / t
+    sample = (f"oracle port of the reference hot path (gradpipe codec {args.codec} on the whole "
+              f"{n}-element gradient, ring_allreduce over p={p} simulated ranks, whole-vector re-compress, "
+              f"mean, SGD) per step, single thread, numpy; the reference has no CNN so forward/backward is "
+              f"excluded (flatters the reference); host: {cpu_model()}, {os.cpu_count()} cpus")
+    return {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": workload_config(args, n, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def workload_config(args, n, N):
+    return {"workload": f"C2 (BASELINE.json configs[1]): CIFAR-10-shaped small CNN, Pipe-SGD width {args.depth}, "
+                        f"{args.codec} ring compression",
+            "model": "SmallCNN 3conv+2fc", "params": n, "global_batch": args.global_batch,
+            "per_gpu_batch": args.global_batch // max(N, 1), "image": [3, 32, 32], "codec": args.codec,
+            "mode": args.mode, "depth": args.depth, "parallelism": f"dp{N}",
+            "l2": "not flushed: each step streams the CNN activations of the per-GPU batch plus the 18.8 MB "
+                  "gradient, weights and slots through HBM"}
+
+
+# ------------------------------------------------------------------ our arm
+
+def our_arm(args, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_03619_b200 import GpuTransport, ProcessGroupTransport
+    from paper_1811_03619_b200.engine import RankEngine, RunConfig
+    from paper_1811_03619_b200.models import FlatModel, build_torch_model
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    N = ws
+    torch.backends.cudnn.benchmark = True
+    if N > 1:
+        ep = ProcessGroupTransport.endpoint(local, max_elems=1 << 26, ctas=args.ctas, timeout_s=60.0)
+    else:
+        tr = GpuTransport(1, max_elems=1 << 10, ctas=args.ctas)
+        ep = tr.endpoint(0)
+    torch.manual_seed(0)  # identical replicas on every rank
+    mod, in_shape, classes = build_torch_model(args.model)
+    fm = FlatModel(mod, dev)
+    n = fm.num_params
+    B = args.global_batch // N
+    total_steps = 2 * (args.warmup + args.steps) + 8
+    cfg = RunConfig(mode=args.mode, iterations=total_steps, learning_rate=0.01, codec=args.codec,
+                    depth=args.depth, batch_size=B, seed=0)
+    g = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    x_host = torch.randn((B, *in_shape), generator=g).pin_memory()
+    y_host = torch.randint(0, classes, (B,), generator=g).pin_memory()
+    x_dev, y_dev = x_host.to(dev), y_host.to(dev)
+    mode = {"e2e": False}
+    x_buf = torch.empty_like(x_dev)
+    y_buf = torch.empty_like(y_dev)
+
+    def batch_fn(r, t):
+        if mode["e2e"]:  # host->device copy of this step's batch from pinned memory
+            x_buf.copy_(x_host, non_blocking=True)
+            y_buf.copy_(y_host, non_blocking=True)
+            return x_buf, y_buf
+        return x_dev, y_dev
+
+    eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True)
+    loss_host = torch.zeros(total_steps + 2, dtype=torch.float32).pin_memory()
+
+    def barrier():
+        if N > 1:
+            dist.barrier()
+
+    def timed_region(t0, steps, e2e):
+        mode["e2e"] = e2e
+        torch.cuda.synchronize(dev)
+        barrier()
+        eng.events.clear()
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(eng.cs)
+        eng.ms.wait_stream(eng.cs)
+        for t in range(t0, t0 + steps):
+            eng.step(t)
+            if e2e:  # device->host read of the step's loss (async into pinned memory)
+                with torch.cuda.stream(eng.cs):
+                    loss_host[t:t + 1].copy_(eng.losses[t:t + 1], non_blocking=True)
+        end_c = torch.cuda.Event(enable_timing=True)
+        end_m = torch.cuda.Event(enable_timing=True)
+        end_c.record(eng.cs)
+        end_m.record(eng.ms)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = max(start.elapsed_time(end_c), start.elapsed_time(end_m))
+        tt = torch.tensor([ms], device=dev)
+        if N > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item()), list(eng.events)
+
+    with torch.cuda.device(dev), torch.cuda.stream(eng.cs):
+        eng.prime(1)
+        t = 1
+        for _ in range(args.warmup):
+            eng.step(t)
+            t += 1
+        with ClockSampler(local) as clk:
+            ms_total, events = timed_region(t, args.steps, e2e=False)
+        t += args.steps
+        for _ in range(2):
+            eng.step(t)
+            t += 1
+        e2e_ms, _ = timed_region(t, args.steps, e2e=True)
+        t += args.steps
+        eng.drain(t - 1)
+        torch.cuda.synchronize(dev)
+    ep._check_errors(n)
+    if any(int(s.t[1].item()) for s in eng.local_status):
+        raise RuntimeError("non-finite gradient in the benchmark run")
+
+    per_step_ms = ms_total / args.steps
+    value = 1e3 / per_step_ms
+    e2e_value = 1e3 / (e2e_ms / args.steps)
+
+    # per-kernel device durations over the timed region (CUDA events on the
+    # launching stream)
+    durs: dict[str, list[float]] = {}
+    for (_, stage, e0, e1, _) in events:
+        durs.setdefault(stage, []).append(e0.elapsed_time(e1))
+    avg = {k: float(np.mean(v)) for k, v in durs.items()}
+    w = {"none": 4, "trunc16": 2, "quant8": 1}[args.codec]
+    q8 = args.codec == "quant8"
+    algo = {  # algorithmic bytes per launch
+        "update": (8 + w) * n,                     # slot read + w read + w write
+        "compress": (12 if q8 else 8) * n,         # (absmax) + read g + write D(C(g))
+        "recompress": (9 if q8 else 4 + w) * n,    # (absmax) + read sum + write payload
+    }
+    from paper_1811_03619_b200.collective import partition_blocks
+    blocks = partition_blocks(n, N)
+    wire = sum(blocks[(rank - s) % N][1] for s in range(N - 1)) * w + \
+        sum(blocks[(rank + 1 - s) % N][1] for s in range(N - 1)) * w if N > 1 else 0
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    kernels = {}
+    for k in ("update", "compress", "recompress", "ring"):
+        if k in avg:
+            kernels[k] = {"avg_ms": avg[k]}
+            if k in algo:
+                kernels[k]["hbm_gbs"] = algo[k] / (avg[k] * 1e-3) / 1e9
+    if N > 1:
+        kernels["ring"]["wire_bytes"] = wire
+        kernels["ring"]["nvlink_gbs"] = wire / (avg["ring"] * 1e-3) / 1e9
+        dom = "ring"
+        roof = {"kernel": "ring_allreduce_kernel (fused decode+add+encode+P2P push)", "bound": "nvlink",
+                "achieved": kernels["ring"]["nvlink_gbs"], "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                "frac": kernels["ring"]["nvlink_gbs"] / NVLINK_PEAK_GBS, "traffic": None,
+                "peak_source": "B200_PROFILING.md measured peer copy (MEASURED_PEAKS.json has no NVLink figure)",
+                "algorithmic_bytes_per_launch": wire}
+    else:
+        dom = max(("update", "compress", "recompress"), key=lambda k: avg.get(k, 0.0))
+        roof = {"kernel": {"update": "consume_update_kernel", "compress": "roundtrip_kernel",
+                           "recompress": "encode_kernel"}[dom],
+                "bound": "hbm", "achieved": kernels[dom]["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": kernels[dom]["hbm_gbs"] / hbm_peak, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                "algorithmic_bytes_per_launch": algo[dom]}
+    per_iter_launches = 1 + (2 if q8 else 1) + (1 if N > 1 else 0) + (2 if q8 else 1)
+
+    allreduce = None
+    if N > 1 and not args.no_allreduce_sweep:
+        allreduce = ring_vs_nccl(ep, args.codec, N, dev, [n, 1 << 26])
+
+    line = None
+    if rank == 0:
+        h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
+        line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": N, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (random CIFAR-shaped images/labels, random-init weights)",
+                "config": workload_config(args, n, N),
+                "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d * N,
+                        "d2h_bytes_per_step": 4 * N,
+                        "how": "same engine; every step copies the rank's batch from pinned host memory and "
+                               "reads the loss back"},
+                "gpu_launches": per_iter_launches * args.steps,
+                "roofline": roof, "kernels": kernels, "clocks": clk.summary(),
+                "samples_per_s": value * args.global_batch}
+        if allreduce:
+            line["allreduce"] = allreduce
+        line["timing_model"] = timing_model(avg, n, N, w)
+    return line
+
+
+def ring_vs_nccl(ep, codec, N, dev, sizes):
+    import torch
+    import torch.distributed as dist
+    from paper_1811_03619_b200.collective import allreduce_into, endpoint_wait
+    out = []
+    s = torch.cuda.Stream(dev)
+    for n in sizes:
+        x = torch.randn(n, device=dev)
+        y = torch.empty_like(x)
+        res = {"n": n, "bytes_fp32": 4 * n}
+        for name in (codec, "none", "nccl"):
+            if name in res:
+                continue
+            it = 20 if n < (1 << 24) else 8
+
+            def run():
+                if name == "nccl":
+                    with torch.cuda.stream(s):
+                        dist.all_reduce(y)
+                else:
+                    allreduce_into(x, y, ep, name, 0, s)
+
+            for _ in range(3):
+                run()
+            s.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(it):
+                run()
+            b.record(s)
+            b.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / it], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            if name != "nccl":
+                endpoint_wait(ep, n, s)
+            res[name] = {"ms": ms, "busbw_gbs": 2 * (N - 1) / N * 4 * n / (ms * 1e-3) / 1e9}
+        out.append(res)
+    return out
+
+
+def timing_model(avg, n, N, w):
+    """Paper Eq. (4)/(5) (timing.py:109-132) with GPU-measured stage times:
+    pipe iteration = max(update + compute, comm)."""
+    upd = avg.get("update", 0.0) + avg.get("compress", 0.0)
+    comp = avg.get("backward", 0.0)
+    comm = avg.get("allreduce", 0.0)
+    return {"update_ms": upd, "compute_ms": comp, "comm_ms": comm,
+            "predicted_pipe_ms": max(upd + comp, comm), "predicted_sync_ms": upd + comp + comm,
+            "bound": "compute" if upd + comp >= comm else "communication"}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_info()
+    if ws != args.gpus and ws > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+    if args.impl == "reference":
+        line = reference_arm(args, ws, rank)
+        if line:
+            print(json.dumps(line), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = our_arm(args, ws, rank, local)
+    if line is not None and not args.no_cpu_baseline and ws == 1:
+        from oracle import codec as OC
+        codec = {"none": OC.NONE, "trunc16": OC.TRUNC16, "quant8": OC.QUANT8}[args.codec]
+        v, k, dt = cpu_path_rate(line["config"]["params"], 1, codec, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": v, "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": (f"{k} iterations ({dt:.1f} s) of the oracle port of the reference hot path on the "
+                       f"{line['config']['params']}-element gradient (codec, p=1 ring, re-compress, mean, SGD; "
+                       f"no CNN fwd/bwd: the reference has none); host {cpu_model()}")}
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -131,7 +131,7 @@ uint32_t pick_chunk(uint64_t n, int p, int G) {
 int check_common(gp_comm* c, uint64_t n, int codec) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   if (codec < 0 || codec > 2) return fail(GP_ERR_ARG, "unknown codec " + std::to_string(codec));
-  if (n > c->max_elems)
+  if (n > c->max_elems && c->world > 1)
     return fail(GP_ERR_ARG, "vector of " + std::to_string(n) + " elems exceeds communicator capacity " +
                                 std::to_string(c->max_elems));
   if (n >= (1ull << 32) * (uint64_t)c->world) return fail(GP_ERR_ARG, "block exceeds 2^32 elements");

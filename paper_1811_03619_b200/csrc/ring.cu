@@ -76,14 +76,23 @@ __device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
   return *(volatile unsigned long long*)&ctl->abort >= P.seq;
 }
 
-// Lane 0 spins until *f >= seq. Returns false on timeout or abort.
+// Lane 0 spins until *f >= seq. Returns false on timeout or abort. Polls
+// with relaxed loads and a short exponential back-off (thousands of warps
+// poll at once; acquire loads in a tight loop would flood L2), then takes
+// the acquire with one final ld.acquire.
 __device__ bool spin_flag(const uint64_t* f, const RingParams& P, const RankCtx& R, Ctl* ctl,
                           ErrWord* err, int phase, int step, int block) {
   if (ld_acquire_sys(f) >= P.seq) return true;
   const uint64_t t0 = globaltimer();
+  uint32_t ns = 32;
   for (uint32_t it = 1;; ++it) {
-    if (ld_acquire_sys(f) >= P.seq) return true;
-    if ((it & 127u) == 0) {
+    if (ld_relaxed_sys(f) >= P.seq) {
+      (void)ld_acquire_sys(f);
+      return true;
+    }
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if ((it & 63u) == 0) {
       if (aborted(P, ctl)) {
         latch_error(err, kErrTimeout, phase, step, block, R.rank, 1 /* peer aborted */);
         return false;

@@ -202,10 +202,11 @@ class RankEngine:
             self.sync_slot = _Slot(Codec.NONE, self.summed.view(torch.uint8), CodecStatus(self.dev))
             self.local_status = [CodecStatus(self.dev) for _ in range(K)]
             self.slot_nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
-            self.losses = torch.zeros(config.iterations + 1, dtype=torch.float32, device=self.dev)
+            self.losses = torch.zeros(config.iterations + 2, dtype=torch.float32, device=self.dev)
         self.ev_local = [torch.cuda.Event() for _ in range(K)]
         self.buffer = GradientBuffer(K)
         self.iter_done: dict[int, torch.cuda.Event] = {}
+        self._pending = None
         self.early_params: list = []
         self.eval_points: list = []
         self.updates_seen = 0
@@ -266,6 +267,7 @@ class RankEngine:
         self.ms.wait_event(self.ev_local[i])
         e0 = self._ev(self.ms) if self.tracing else None
         allreduce_into(self.local[i], self.summed, self.ep, self.cfg.codec, t, self.ms)
+        e1 = self._ev(self.ms) if self.tracing else None
         if requant:
             slot = self.slots[i]
             encode_async(self.summed, self.cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
@@ -275,25 +277,18 @@ class RankEngine:
         ready.record(self.ms)
         if self.tracing:
             self._rec(t, STAGE_ALLREDUCE, e0, ready)
+            self._rec(t, "ring", e0, e1)
+            if requant:
+                self._rec(t, "recompress", e1, ready)
         self.buffer.put(t, slot, ready)
         return slot
 
     # ------------------------------------------------------------------ loops
-    def sync_phase(self, t0: int, t1: int) -> None:
-        """d_sync (engine.py:340-375): update(pending) -> compute -> ring."""
-        pending = None
-        for t in range(t0, t1 + 1):
-            if pending is not None:
-                self._consume(self.buffer.take(pending, self.cs), pending, t)
-            self._compute_local(t)
-            self._communicate(t, requant=False)
-            pending = t
-            self._mark(t)
-        if pending is not None:
-            self._consume(self.buffer.take(pending, self.cs), pending, pending + 1)
-
-    def pipe_phase(self, t0: int, t1: int) -> None:
-        """pipe_sgd (engine.py:379-448) with zero-primed slots and K-drain."""
+    # Incremental API (used by bench.py to time exactly K steady-state steps):
+    #   pipe: prime(t0); step(t) for t0..t1; drain(t1)
+    #   sync: step_sync(t) for t0..t1; drain_sync()
+    def prime(self, t0: int) -> None:
+        """Zero slots for tags t0-K .. t0-1 (engine.py:382-388)."""
         K = self.K
         for tag in range(t0 - K, t0):
             slot = self.slots[tag % K]
@@ -302,13 +297,44 @@ class RankEngine:
             ev = torch.cuda.Event()
             ev.record(self.cs)
             self.buffer.put(tag, slot, ev)
+
+    def step(self, t: int) -> None:
+        """One pipelined iteration: update with slot t-K, compute t, ring t."""
+        self._consume(self.buffer.take(t - self.K, self.cs), t - self.K, t)
+        self._compute_local(t)
+        self._communicate(t, requant=True)
+        self._mark(t)
+
+    def drain(self, t1: int) -> None:
+        for tag in range(t1 - self.K + 1, t1 + 1):
+            self._consume(self.buffer.take(tag, self.cs), tag, tag + self.K)
+
+    def step_sync(self, t: int) -> None:
+        if self._pending is not None:
+            self._consume(self.buffer.take(self._pending, self.cs), self._pending, t)
+        self._compute_local(t)
+        self._communicate(t, requant=False)
+        self._pending = t
+        self._mark(t)
+
+    def drain_sync(self) -> None:
+        if self._pending is not None:
+            self._consume(self.buffer.take(self._pending, self.cs), self._pending, self._pending + 1)
+        self._pending = None
+
+    def sync_phase(self, t0: int, t1: int) -> None:
+        """d_sync (engine.py:340-375): update(pending) -> compute -> ring."""
+        self._pending = None
         for t in range(t0, t1 + 1):
-            self._consume(self.buffer.take(t - K, self.cs), t - K, t)
-            self._compute_local(t)
-            self._communicate(t, requant=True)
-            self._mark(t)
-        for tag in range(t1 - K + 1, t1 + 1):
-            self._consume(self.buffer.take(tag, self.cs), tag, tag + K)
+            self.step_sync(t)
+        self.drain_sync()
+
+    def pipe_phase(self, t0: int, t1: int) -> None:
+        """pipe_sgd (engine.py:379-448) with zero-primed slots and K-drain."""
+        self.prime(t0)
+        for t in range(t0, t1 + 1):
+            self.step(t)
+        self.drain(t1)
 
     def _mark(self, t):
         e = torch.cuda.Event(enable_timing=True)
