@@ -120,6 +120,19 @@ def dist_info():
     return ws, rank, local
 
 
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank float over the default process group (CPU tensor for
+    gloo, device tensor for nccl); the value itself when not distributed."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    dev = device if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_model():
     try:
         return [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
@@ -285,10 +298,7 @@ def our_arm(args, ws, rank, local):
         torch.cuda.synchronize(dev)
         barrier()
         ms = max(start.elapsed_time(end_c), start.elapsed_time(end_m))
-        tt = torch.tensor([ms], device=dev)
-        if N > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item()), list(eng.events)
+        return max_over_ranks(ms, dev), list(eng.events)
 
     with torch.cuda.device(dev), torch.cuda.stream(eng.cs):
         eng.prime(1)

@@ -1,0 +1,216 @@
+"""The paper's analytic timing model (Eqs. 2-7), plus GPU calibration.
+
+Same names and float64 formulas as /root/reference/pkg/src/gradpipe/timing.py
+(StageTimes :21-47, ClusterParams :50-85, t_sync_total Eq. 2 :97-99,
+t_pipe_ideal Eq. 3 :102-106, t_pipe_limited Eq. 4 :109-116, ring_comm_time
+Eq. 5 :119-132, segmented_comm_time / t_pipe_seq / t_pipe_segmented Eq. 6
+:135-188, star_comm_time :155-170, scaling_efficiency Eq. 7 :191-200,
+recommend_config :210-232). `calibrate_nvlink` measures the symbols on the
+B200s instead of on sockets (reference calibrate(): harness.py:513-586):
+alpha from a flag ping-pong, beta from a peer push copy, gamma from the
+fused hop's measured time per byte.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, fields
+
+from .errors import ConfigError
+
+SEQUENTIAL, SEGMENTED = "sequential", "segmented"
+COMPUTE_BOUND, COMM_BOUND = "compute", "communication"
+
+
+def _nonneg(obj, names):
+    for nm in names:
+        if getattr(obj, nm) < 0:
+            raise ConfigError(f"{nm} must be >= 0")
+
+
+@dataclass(frozen=True)
+class StageTimes:
+    """Per-iteration stage durations (s); first_segment_backward <= backward."""
+
+    update: float = 0.0
+    forward: float = 0.0
+    backward: float = 0.0
+    first_segment_backward: float = 0.0
+    comm: float = 0.0
+
+    def __post_init__(self):
+        for f in fields(self):
+            if getattr(self, f.name) < 0:
+                raise ConfigError(f"stage time {f.name} must be >= 0")
+        if self.first_segment_backward > self.backward:
+            raise ConfigError("first-segment backward time cannot exceed the full backward time")
+
+    @property
+    def compute(self) -> float:
+        return self.forward + self.backward
+
+    @property
+    def busy(self) -> float:
+        return self.update + self.compute
+
+
+@dataclass(frozen=True)
+class ClusterParams:
+    """p workers; alpha (s/msg), beta (s/B), gamma_red (s/B), S (s), n (B), L segments."""
+
+    workers: int
+    latency_s: float = 0.0
+    byte_time_s: float = 0.0
+    reduce_time_s: float = 0.0
+    sync_time_s: float = 0.0
+    model_bytes: float = 0.0
+    segments: int = 1
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise ConfigError("need at least one worker")
+        if self.segments < 1:
+            raise ConfigError("need at least one gradient segment")
+        _nonneg(self, ("latency_s", "byte_time_s", "reduce_time_s", "sync_time_s", "model_bytes"))
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    depth: int = 2
+    iterations: int = 1
+
+    def __post_init__(self):
+        if self.depth < 1 or self.iterations < 1:
+            raise ConfigError("pipeline depth and iteration count must be >= 1")
+
+
+def t_sync_total(iterations: int, stages: StageTimes) -> float:
+    """Eq. 2: every stage on the critical path each iteration."""
+    return iterations * (stages.busy + stages.comm)
+
+
+def t_pipe_ideal(iterations: int, depth: int, stages: StageTimes) -> float:
+    """Eq. 3: unlimited resources shorten the run depth-fold."""
+    if depth < 1:
+        raise ConfigError("pipeline depth must be >= 1")
+    return iterations / depth * (stages.busy + stages.comm)
+
+
+def t_pipe_limited(iterations: int, stages: StageTimes) -> float:
+    """Eq. 4: limited resources — the slower of compute and comm dominates."""
+    return iterations * max(stages.busy, stages.comm)
+
+
+def _ring_terms(c: ClusterParams, rounds: int):
+    p = c.workers
+    share = (p - 1) / p
+    return (2 * (p - 1) * rounds * c.latency_s,
+            2 * share * c.model_bytes * c.byte_time_s,
+            share * c.model_bytes * c.reduce_time_s,
+            rounds * c.sync_time_s)
+
+
+def ring_comm_time(params: ClusterParams) -> float:
+    """Eq. 5: 2(p-1)a + 2(p-1)/p n b + (p-1)/p n g + S."""
+    if params.workers == 1:
+        return params.sync_time_s
+    return sum(_ring_terms(params, 1))
+
+
+def segmented_comm_time(params: ClusterParams) -> float:
+    """Eq. 6 comm: latency and sync terms scale with L, byte terms do not."""
+    if params.workers == 1:
+        return params.segments * params.sync_time_s
+    return sum(_ring_terms(params, params.segments))
+
+
+def star_comm_time(params: ClusterParams) -> float:
+    """Parameter-server exchange: (p+1)(a + n b) + p n g + S."""
+    p, n = params.workers, params.model_bytes
+    if p == 1:
+        return params.sync_time_s
+    return (p + 1) * (params.latency_s + n * params.byte_time_s) + p * n * params.reduce_time_s + \
+        params.sync_time_s
+
+
+def t_pipe_seq(iterations: int, stages: StageTimes, params: ClusterParams) -> float:
+    return iterations * max(stages.busy, ring_comm_time(params))
+
+
+def t_pipe_segmented(iterations: int, stages: StageTimes, params: ClusterParams) -> float:
+    head = stages.update + stages.forward + stages.first_segment_backward
+    return iterations * max(head, segmented_comm_time(params))
+
+
+def scaling_efficiency(stages: StageTimes) -> float:
+    """Eq. 7: busy / max(busy, comm); 1 when communication is fully masked."""
+    if stages.busy <= 0:
+        raise ConfigError("scaling efficiency undefined for zero compute time")
+    return stages.busy / max(stages.busy, stages.comm)
+
+
+@dataclass(frozen=True)
+class Recommendation:
+    depth: int
+    comm_mode: str
+    bound: str
+
+
+def recommend_config(stages: StageTimes, params: ClusterParams) -> Recommendation:
+    """Depth 2 always; segment only if compute-bound and it strictly helps."""
+    comm = ring_comm_time(params)
+    busy = stages.busy
+    bound = COMM_BOUND if comm > busy else COMPUTE_BOUND
+    if params.workers == 1 or bound == COMM_BOUND:
+        return Recommendation(2, SEQUENTIAL, bound)
+    seg = max(stages.update + stages.forward + stages.first_segment_backward, segmented_comm_time(params))
+    return Recommendation(2, SEGMENTED if seg < max(busy, comm) else SEQUENTIAL, bound)
+
+
+def predict_iteration_time(stages: StageTimes, params: ClusterParams, mode: str, iterations: int,
+                           depth: int = 2) -> float:
+    """harness.py:667-684: d_sync = busy + comm; pipe = max(busy, comm) with
+    the pipeline fill correction (T + K - 1) / T."""
+    comm = ring_comm_time(params)
+    if mode == "d_sync":
+        return stages.busy + comm
+    return max(stages.busy, comm) * (iterations + depth - 1) / iterations
+
+
+def calibrate_nvlink(devices=(0, 1), nbytes: int = 1 << 30, ctas: int = 148, iters: int = 20000) -> dict:
+    """alpha (one-way flag latency, s) and beta (s/byte of a bidirectional
+    peer push) between two GPUs of this process, with libpipesgd's
+    calibration kernels. Requires two GPUs with peer access."""
+    import torch
+
+    from . import _lib
+    from .transport import GpuTransport
+
+    tr = GpuTransport(2, devices=list(devices), max_elems=1024)
+    a = [torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    b = [torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{d}") for d in devices]
+    st = [torch.cuda.Stream(device=d) for d in devices]
+    ev = []
+    for rep in range(2):
+        for i, d in enumerate(devices):
+            with torch.cuda.device(d):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st[i])
+                _lib.call("gp_calib_p2p_copy", b[1 - i].data_ptr(), a[i].data_ptr(), nbytes, ctas, 0,
+                          st[i].cuda_stream)
+                e1.record(st[i])
+                if rep == 1:
+                    ev.append((e0, e1))
+        for s in st:
+            s.synchronize()
+    beta = max(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3 / nbytes
+    flags = [torch.zeros(4, dtype=torch.int64, device=f"cuda:{d}") for d in devices]
+    ns = [torch.zeros(1, dtype=torch.int64, device=f"cuda:{d}") for d in devices]
+    for i, d in enumerate(devices):
+        with torch.cuda.device(d):
+            _lib.call("gp_calib_pingpong", flags[i].data_ptr(), flags[1 - i].data_ptr(), iters, int(i == 0), 0,
+                      ns[i].data_ptr(), st[i].cuda_stream)
+    for s in st:
+        s.synchronize()
+    alpha = ns[0].item() / iters / 2 / 1e9
+    tr.close()
+    return {"alpha_s": alpha, "beta_s_per_byte": beta, "push_gbs": 1 / beta / 1e9}

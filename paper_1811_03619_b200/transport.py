@@ -307,6 +307,31 @@ class EmulatedTransport:
             self._comm = None
 
 
+def exchange_handles(handle: bytes, max_elems: int, device: int, group=None) -> bytes:
+    """All-gather every rank's 64-byte inbox IPC handle over the process
+    group (any backend) and validate that the communicator geometry agrees;
+    returns the rank-ordered handle blob gp_comm_connect_ipc expects."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (bytes(handle), int(max_elems), int(device), _host_id()), group=group)
+    if len({g[1] for g in gathered}) != 1:
+        raise ConfigError("all ranks must create the transport with the same max_elems")
+    if len({g[3] for g in gathered}) != 1:
+        raise ConfigError("ProcessGroupTransport spans one node only (NVLink peer memory)")
+    if len({g[2] for g in gathered}) != world:
+        raise ConfigError("ProcessGroupTransport needs a distinct GPU per rank")
+    if any(len(g[0]) != 64 for g in gathered):
+        raise ConfigError("malformed IPC handle")
+    return b"".join(g[0] for g in gathered)
+
+
+def _host_id() -> str:
+    import socket
+    return socket.gethostname()
+
+
 class ProcessGroupTransport:
     """One rank per process (torchrun), inboxes mapped through CUDA IPC.
 
@@ -328,13 +353,7 @@ class ProcessGroupTransport:
         if world > 1:
             h = ctypes.create_string_buffer(64)
             _lib.call("gp_comm_ipc_handle", comm, h)
-            gathered = [None] * world
-            dist.all_gather_object(gathered, (h.raw, int(max_elems), int(device)), group=group)
-            if len({g[1] for g in gathered}) != 1:
-                raise ConfigError("all ranks must create the transport with the same max_elems")
-            if len({g[2] for g in gathered}) != world:
-                raise ConfigError("ProcessGroupTransport needs a distinct GPU per rank")
-            blob = b"".join(g[0] for g in gathered)
+            blob = exchange_handles(h.raw, int(max_elems), int(device), group)
             _lib.call("gp_comm_connect_ipc", comm, blob)
             dist.barrier(group)
         return GpuEndpoint(rank, world, torch.device("cuda", device), comm, timeout_s)
