@@ -23,7 +23,7 @@ GP_PHASE_RS, GP_PHASE_AG, GP_PHASE_BARRIER = 0, 1, 2
 # Every symbol include/pipesgd.h declares (checked by tests/test_cabi.py).
 EXPORTS = (
     "gp_comm_create", "gp_comm_create_emulated", "gp_comm_ipc_handle", "gp_comm_connect_ipc",
-    "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_info", "gp_comm_destroy",
+    "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_info", "gp_comm_destroy",
     "gp_allreduce", "gp_allreduce_emulated", "gp_comm_poll_error", "gp_get_stats",
     "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update",
     "gp_calib_p2p_copy", "gp_calib_pingpong", "gp_last_error_string", "gp_version",
@@ -50,6 +50,7 @@ _SIGS = {
     "gp_comm_connect_ipc": (_i, [_vp, ctypes.c_char_p]),
     "gp_comm_connect_local": (_i, [ctypes.POINTER(_vp), _i]),
     "gp_comm_set_tuning": (_i, [_vp, _i, _d]),
+    "gp_comm_set_trace": (_i, [_vp, _vp]),
     "gp_comm_info": (_i, [_vp, ctypes.POINTER(ctypes.c_int64)]),
     "gp_comm_destroy": (_i, [_vp]),
     "gp_allreduce": (_i, [_vp, _vp, _vp, _u64, _i, _u32, _vp]),

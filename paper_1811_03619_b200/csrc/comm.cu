@@ -70,10 +70,10 @@ struct gp_comm {
   bool ipc_opened[kMaxRanks] = {};
   bool connected = false;
   uint32_t seq = 0;
-  unsigned long long bar_total = 0;
   int G = 0;
   double timeout_s = 30.0;
   gp_stats stats[kMaxRanks] = {};
+  unsigned long long* trace = nullptr;  // optional device timeline buffer
 };
 
 namespace {
@@ -268,6 +268,12 @@ int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
   return GP_OK;
 }
 
+int gp_comm_set_trace(gp_comm* c, void* device_buffer) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  c->trace = static_cast<unsigned long long*>(device_buffer);
+  return GP_OK;
+}
+
 int gp_comm_info(gp_comm* c, int64_t* o) {
   if (!c || !o) return fail(GP_ERR_ARG, "null argument");
   o[0] = c->rank; o[1] = c->world; o[2] = c->device; o[3] = (int64_t)c->max_elems;
@@ -302,11 +308,11 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint6
   P.p = p;
   P.codec = codec;
   P.G = c->G;
-  P.seq = ++c->seq;
+  ++c->seq;  // host-side count (info only); the kernel numbers calls on the device
   P.iteration = iteration;
   P.chunk = pick_chunk(n, p, c->G);
-  P.bar_base = c->bar_total;
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
+  P.trace = c->trace;
   for (int i = 0; i < c->nlocal; ++i) {
     RankCtx& R = P.rk[i];
     R.x = ins[i];
@@ -318,7 +324,6 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint6
   cudaError_t e;
   launch_ring(P, c->nlocal, st, &e);
   if (e != cudaSuccess) return cuda_fail(e, "ring kernel launch");
-  if (codec == GP_CODEC_QUANT8) c->bar_total += (unsigned long long)p * c->G * kRingWarps;
   for (int i = 0; i < c->nlocal; ++i) account(c->stats[i], P.rk[i].rank, p, n, codec);
   return GP_OK;
 }

@@ -28,6 +28,8 @@
 // push over NVSwitch (the bytes the ring would forward, one hop not p-1).
 // Emulation: with nlocal == p the same kernel runs all p ranks on one GPU
 // in one cooperative launch (CTA group = rank) for parity tests at p > #GPUs.
+#include <cstdlib>
+
 #include "codec.cuh"
 #include "ring.cuh"
 
@@ -37,6 +39,11 @@ namespace {
 
 constexpr int kWarps = kRingThreads / 32;
 constexpr uint64_t kBatch = 1024;  // elements per warp per batch (32 lanes x U x E)
+
+// This call's sequence number, read from the rank's control block at entry.
+// It lives on the device (not in the launch parameters) so a launch can be
+// captured once in a CUDA graph and replayed: every replay is a new call.
+__shared__ uint32_t s_seq;
 
 struct Blk {
   uint64_t start, len, A;
@@ -67,13 +74,13 @@ __device__ __forceinline__ uint8_t* slot_ptr(uint8_t* inbox, const Layout& L, in
 __device__ void broadcast_abort(const RingParams& P, const RankCtx& R) {
   for (int q = 0; q < P.p; ++q) {
     Ctl* c = reinterpret_cast<Ctl*>(R.peer[q] + P.L.off_ctl);
-    atomicMax(&c->abort, (unsigned long long)P.seq);
+    atomicMax(&c->abort, (unsigned long long)s_seq);
   }
   fence_sys();
 }
 
 __device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
-  return *(volatile unsigned long long*)&ctl->abort >= P.seq;
+  return *(volatile unsigned long long*)&ctl->abort >= s_seq;
 }
 
 // Lane 0 spins until *f >= seq. Returns false on timeout or abort. Polls
@@ -82,11 +89,11 @@ __device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
 // the acquire with one final ld.acquire.
 __device__ bool spin_flag(const uint64_t* f, const RingParams& P, const RankCtx& R, Ctl* ctl,
                           ErrWord* err, int phase, int step, int block) {
-  if (ld_acquire_sys(f) >= P.seq) return true;
+  if (ld_acquire_sys(f) >= s_seq) return true;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
   for (uint32_t it = 1;; ++it) {
-    if (ld_relaxed_sys(f) >= P.seq) {
+    if (ld_relaxed_sys(f) >= s_seq) {
       (void)ld_acquire_sys(f);
       return true;
     }
@@ -134,7 +141,7 @@ __device__ bool warp_await(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrW
 __device__ __forceinline__ void write_hdr(const RingParams& P, uint8_t* dst, int slot, int block,
                                           uint64_t len, float scale) {
   SlotHdr* h = hdr_ptr(dst, P.L, slot);
-  h->seq = P.seq;
+  h->seq = s_seq;
   h->iteration = P.iteration;
   h->block = (uint32_t)block;
   h->n_elems = (uint32_t)len;
@@ -148,7 +155,7 @@ __device__ __forceinline__ void warp_publish(const RingParams& P, uint8_t* dst, 
   __syncwarp();
   if (lane_id() == 0) {
     write_hdr(P, dst, slot, block, len, scale);
-    st_release_sys(flag_ptr(dst, P.L, slot, c), P.seq);  // release: orders the warp's stores
+    st_release_sys(flag_ptr(dst, P.L, slot, c), s_seq);  // release: orders the warp's stores
   }
 }
 
@@ -160,7 +167,7 @@ __device__ __forceinline__ void warp_publish_all(const RingParams& P, const Rank
     for (int d = 1; d < P.p; ++d) write_hdr(P, R.peer[(R.rank + d) % P.p], ag_slot(P.p, b), b, len, scale);
     fence_sys();  // one system fence, then relaxed-cost releases to every peer
     for (int d = 1; d < P.p; ++d)
-      st_release_sys(flag_ptr(R.peer[(R.rank + d) % P.p], P.L, ag_slot(P.p, b), c), P.seq);
+      st_release_sys(flag_ptr(R.peer[(R.rank + d) % P.p], P.L, ag_slot(P.p, b), c), s_seq);
   }
 }
 
@@ -172,10 +179,10 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
   int ok = 1;
   float v = 0.f;
   if (lane_id() == 0) {
-    atomicMax(&ctl->maxslot[k], ((unsigned long long)P.seq << 32) | m);
+    atomicMax(&ctl->maxslot[k], ((unsigned long long)s_seq << 32) | m);
     __threadfence();
     atomicAdd(&ctl->bar, 1ull);
-    const unsigned long long target = P.bar_base + (unsigned long long)(k + 1) * P.G * kWarps;
+    const unsigned long long target = (unsigned long long)(k + 1) * P.G * kWarps;
     const uint64_t t0 = globaltimer();
     for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->bar)) < target; ++it) {
       __nanosleep(64);
@@ -190,7 +197,7 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
       }
     }
     const unsigned long long w = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->maxslot[k]));
-    v = ((uint32_t)(w >> 32) == P.seq) ? __uint_as_float((uint32_t)w) : 0.f;
+    v = ((uint32_t)(w >> 32) == s_seq) ? __uint_as_float((uint32_t)w) : 0.f;
   }
   __syncwarp();
   ok = __shfl_sync(0xffffffffu, ok, 0);
@@ -224,6 +231,12 @@ __device__ __forceinline__ void for_groups(const RingParams& P, const Blk& B, ui
   }
 }
 
+// Optional timeline (debug/profiling): lane 0 of warp `wid` stamps slot k.
+__device__ __forceinline__ void stamp(const RingParams& P, uint32_t wid, int lrank, int k) {
+  if (P.trace != nullptr && (threadIdx.x & 31) == 0)
+    P.trace[((uint64_t)lrank * P.G * kWarps + wid) * kTraceSlots + k] = globaltimer();
+}
+
 template <int E>
 struct XIn {
   FV<E> x;
@@ -233,7 +246,7 @@ struct XIn {
 }  // namespace
 
 template <int C>
-__global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
+__device__ __forceinline__ void ring_body(const RingParams& P) {
   constexpr int E = CodecT<C>::E;
   const int G = P.G;
   const int lr = blockIdx.x / G;
@@ -246,6 +259,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
   const float* __restrict__ x = R.x;
   float* out = R.out;
   int bad = 0;
+  stamp(P, wid, lr, 0);
 
   // ---- reduce-scatter step 0, send side: C(x_r[block r]) -> succ slot 0
   {
@@ -272,6 +286,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhRS, 0, r, r, 0);
     bad = 0;
+    stamp(P, wid, lr, 1);
   }
 
   // ---- reduce-scatter steps: fold block (r-s-1)%p, forward (or own it)
@@ -299,6 +314,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
       for (uint32_t c = wid; c < B.nch; c += W) {
         float sin;
         if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
+        if (c == wid) stamp(P, wid, lr, 2 + 2 * s);
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                         emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(v.x, decode_v<C>(v.in, sin)), q, bad), 0.f);
@@ -312,6 +328,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
       for (uint32_t c = wid; c < B.nch; c += W) {
         float sin;
         if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
+        if (c == wid) stamp(P, wid, lr, 2 + 2 * s);
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
                         const FV<E> acc = add_v(v.x, decode_v<C>(v.in, sin));
@@ -338,6 +355,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
       latch_error(err, kErrNonFinite, last ? kPhAG : kPhRS, last ? 0 : s + 1, b, r, 0);
     bad = 0;
+    stamp(P, wid, lr, 3 + 2 * s);
   }
 
   // ---- allgather, receive side: decode every other owner's bytes
@@ -349,6 +367,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     for (uint32_t c = wid; c < B.nch; c += W) {
       float sin;
       if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) return;
+      if (k == 1 && c == wid) stamp(P, wid, lr, 18);
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
                       return load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
@@ -356,6 +375,28 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const uint4& v) {
                       store_fv<E>(out, g0, lo, hi, decode_v<C>(v, sin));
                     });
+    }
+  }
+  stamp(P, wid, lr, 19);
+}
+
+template <int C>
+__global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
+  const int lr = blockIdx.x / P.G;
+  Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
+  if (threadIdx.x == 0) s_seq = (uint32_t)(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)) + 1);
+  __syncthreads();
+  ring_body<C>(P);  // returns early (per warp) on timeout / abort / header mismatch
+  // Last warp of this rank to leave closes the call: counters reset, calls
+  // advanced. The next call on this stream starts only after this kernel.
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long prev = atomicAdd(&ctl->exits, 1ull);
+    if (prev == (unsigned long long)P.G * kWarps - 1) {
+      ctl->exits = 0;
+      ctl->bar = 0;
+      __threadfence();
+      atomicExch(&ctl->calls, (unsigned long long)s_seq);
     }
   }
 }
@@ -366,7 +407,20 @@ void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError
   const void* fn = P.codec == kNone      ? (const void*)ring_allreduce_kernel<kNone>
                    : P.codec == kTrunc16 ? (const void*)ring_allreduce_kernel<kTrunc16>
                                          : (const void*)ring_allreduce_kernel<kQuant8>;
-  *err = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, stream);
+  // Emulated rings (nlocal > 1) need every CTA co-resident: cooperative
+  // launch. A single rank per GPU only needs its G <= #SM CTAs to become
+  // resident eventually (no CTA waits on a CTA of its own launch except the
+  // quant8 rank barrier, and G CTAs always fit once other kernels drain), so
+  // it can take the cheaper ordinary launch.
+  static const int mode = [] {
+    const char* e = std::getenv("PIPESGD_LAUNCH");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (nlocal > 1 || mode == 0) {
+    *err = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, stream);
+  } else {
+    *err = cudaLaunchKernel(fn, grid, block, args, 0, stream);
+  }
 }
 
 int ring_warps_per_cta() { return kWarps; }

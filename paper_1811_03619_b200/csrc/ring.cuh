@@ -22,9 +22,11 @@ struct Layout {
 };
 
 struct Ctl {                   // rank-private control block
-  unsigned long long bar;      // monotonic barrier arrival counter
-  unsigned long long abort;    // == seq when this call aborted
+  unsigned long long bar;      // quant8 barrier arrivals in the current call
+  unsigned long long abort;    // >= seq when the current call aborted
   unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier
+  unsigned long long calls;    // completed calls; this call's sequence number is calls + 1
+  unsigned long long exits;    // warps that finished the current call
 };
 
 struct SlotHdr {               // written by the sender before each chunk flag
@@ -45,12 +47,15 @@ struct RingParams {
   RankCtx rk[kMaxRanks];       // one entry per rank in this launch (1, or p when emulated)
   Layout L;
   uint64_t n;
-  unsigned long long bar_base; // Ctl::bar value at entry
   uint64_t timeout_ns;
-  uint32_t seq, iteration;
+  uint32_t iteration;
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
   int p, codec, G;             // world size, codec tag, CTAs per rank (16 warp workers each)
+  unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
+
+constexpr int kTraceSlots = 20;  // [0] start, [1] step-0 send done, [2+2s] step s first chunk
+                                 // in, [3+2s] step s done, [18] allgather first in, [19] end
 
 __host__ __device__ inline int rs_slot(int s) { return s; }
 __host__ __device__ inline int ag_slot(int p, int b) { return p - 1 + b; }

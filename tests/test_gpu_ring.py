@@ -171,3 +171,44 @@ def test_p2p_timeout_produces_diagnostic(P):
             P.ring_allreduce(np.ones(8, np.float32), 0, 2, tr.endpoint(0))
     finally:
         tr.close()
+
+
+@multigpu
+def test_p2p_ring_in_cuda_graph_replays_bit_exact(P):
+    """The call sequence number lives on the device, so one captured launch
+    can be replayed as many calls (what graph-captured training steps need)."""
+    from paper_1811_03619_b200.collective import allreduce_into
+    p, n = 2, 300_007
+    g = np.random.default_rng(5)
+    ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
+    want = {c: OR.ring_allreduce_all(ins, int(c)).outputs[0] for c in P.Codec}
+    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=n)
+
+    def op(r, ep):
+        dev = torch.device("cuda", r)
+        with torch.cuda.device(dev):
+            x = torch.from_numpy(ins[r]).to(dev)
+            outs = {c: torch.empty_like(x) for c in P.Codec}
+            s = torch.cuda.Stream(dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s, capture_error_mode="thread_local"):
+                for c in P.Codec:
+                    allreduce_into(x, outs[c], ep, c, 1, s)
+            got = []
+            for _ in range(4):
+                for o in outs.values():
+                    o.zero_()
+                graph.replay()
+                torch.cuda.synchronize(dev)
+                got.append({c: o.cpu().numpy() for c, o in outs.items()})
+            ep._check_errors(n)
+            return got
+
+    try:
+        res = run_ranks(tr, op)
+        for r in range(p):
+            for rep in res[r]:
+                for c in P.Codec:
+                    assert_bits_equal(rep[c], want[c], f"rank {r} {c.name}")
+    finally:
+        tr.close()

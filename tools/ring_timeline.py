@@ -1,0 +1,73 @@
+"""Per-warp timeline of one ring call (torchrun, one process per GPU).
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/ring_timeline.py --n 4194304 --codec trunc16
+
+Prints, for rank 0, percentiles over warps of each phase stamp relative to
+the earliest kernel start on that GPU (us), plus the CUDA-event time of the
+same call, so launch overhead / flag latency / streaming time separate.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1811_03619_b200 import Codec, ProcessGroupTransport, _lib  # noqa: E402
+from paper_1811_03619_b200.collective import allreduce_into, endpoint_wait  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--numel", type=int, default=1 << 22)
+ap.add_argument("--codec", default="trunc16")
+ap.add_argument("--ctas", type=int, default=0)
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+local = int(os.environ.get("LOCAL_RANK", 0))
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+rank, p = dist.get_rank(), dist.get_world_size()
+ep = ProcessGroupTransport.endpoint(local, max_elems=a.numel, ctas=a.ctas, timeout_s=20)
+G = ep.info()["ctas"]
+W = G * 16
+tr = torch.zeros(W * 20, dtype=torch.int64, device="cuda")
+x = torch.randn(a.numel, device="cuda")
+y = torch.empty_like(x)
+codec = Codec.parse(a.codec)
+s = torch.cuda.current_stream()
+for _ in range(3):
+    allreduce_into(x, y, ep, codec, 0, s)
+endpoint_wait(ep, a.numel, s)
+res = []
+for rep in range(a.reps):
+    tr.zero_()
+    _lib.call("gp_comm_set_trace", ep._comm, tr.data_ptr())
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    allreduce_into(x, y, ep, codec, 0, s)
+    e1.record(s)
+    endpoint_wait(ep, a.numel, s)
+    _lib.call("gp_comm_set_trace", ep._comm, None)
+    t = tr.view(W, 20).cpu().numpy().astype(np.int64)
+    t0 = t[:, 0][t[:, 0] > 0].min()
+    names = {1: "send0_done", 2: "s0_first_in", 3: "s0_done", 18: "ag_first_in", 19: "end"}
+    for s_ in range(1, p - 1):
+        names[2 + 2 * s_] = f"s{s_}_first_in"
+        names[3 + 2 * s_] = f"s{s_}_done"
+    row = {"event_us": e0.elapsed_time(e1) * 1e3, "kernel_span_us": (t[:, 19].max() - t0) / 1e3,
+           "start_spread_us": (t[:, 0][t[:, 0] > 0].max() - t0) / 1e3}
+    for k, nm in sorted(names.items()):
+        v = t[:, k]
+        v = v[v > 0]
+        if v.size:
+            q = np.percentile((v - t0) / 1e3, [0, 50, 90, 100])
+            row[nm] = [round(float(z), 1) for z in q]
+    res.append(row)
+if rank == 0:
+    print(json.dumps({"n": a.numel, "codec": a.codec, "p": p, "ctas": G, "reps": res[-2:]}, indent=1))
+dist.barrier()
+dist.destroy_process_group()
