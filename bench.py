@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--ctas", type=int, default=32,
                     help="CTAs the ring kernel may occupy per GPU (the rest keep computing)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--channels-last", type=int, default=1,
+                    help="feed NHWC activations to cuDNN (no NCHW<->NHWC transposes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-allreduce-sweep", action="store_true")
     return ap.parse_args()
@@ -259,9 +261,11 @@ def our_arm(args, ws, rank, local):
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x_host = torch.randn((B, *in_shape), generator=g).pin_memory()
     y_host = torch.randint(0, classes, (B,), generator=g).pin_memory()
+    if args.channels_last and len(in_shape) == 3:
+        x_host = x_host.contiguous(memory_format=torch.channels_last).pin_memory()
     x_dev, y_dev = x_host.to(dev), y_host.to(dev)
     mode = {"e2e": False}
-    x_buf = torch.empty_like(x_dev)
+    x_buf = torch.empty_like(x_dev)  # keeps x_dev's memory format
     y_buf = torch.empty_like(y_dev)
 
     def batch_fn(r, t):

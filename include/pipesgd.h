@@ -112,6 +112,9 @@ int gp_consume_update(float* params, int codec, const void* slot, const float* s
 
 /* ---- calibration (timing-model alpha/beta on NVLink) ------------------- */
 int gp_calib_p2p_copy(void* dst, const void* src, uint64_t bytes, int ctas, int pull, void* stream);
+/* mode: bit0 pull, bit1 contiguous chunks from a device counter, bit2 release a flag per chunk */
+int gp_calib_p2p_copy_ex(void* dst, const void* src, uint64_t bytes, int ctas, int mode, uint64_t chunk_bytes,
+                         void* counter /* device u64, zeroed */, void* flags /* device u64[] */, void* stream);
 int gp_calib_pingpong(void* mine, void* theirs, int iters, int initiator, uint64_t base,
                       void* ns_out /* device u64 */, void* stream);
 

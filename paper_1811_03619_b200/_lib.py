@@ -14,7 +14,7 @@ import threading
 from .errors import NativeLibraryError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpipesgd.so")
+LIB_PATH = os.environ.get("PIPESGD_LIB") or os.path.join(HERE, "libpipesgd.so")
 
 GP_OK = 0
 GP_FAIL_NONFINITE, GP_FAIL_TIMEOUT, GP_FAIL_HEADER = 1, 2, 3
@@ -26,7 +26,7 @@ EXPORTS = (
     "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_info", "gp_comm_destroy",
     "gp_allreduce", "gp_allreduce_emulated", "gp_comm_poll_error", "gp_get_stats",
     "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update",
-    "gp_calib_p2p_copy", "gp_calib_pingpong", "gp_last_error_string", "gp_version",
+    "gp_calib_p2p_copy", "gp_calib_p2p_copy_ex", "gp_calib_pingpong", "gp_last_error_string", "gp_version",
 )
 
 
@@ -63,6 +63,7 @@ _SIGS = {
     "gp_roundtrip": (_i, [_i, _vp, _vp, _u64, _vp, _vp]),
     "gp_consume_update": (_i, [_vp, _i, _vp, _vp, _u64, _f, _i, _vp]),
     "gp_calib_p2p_copy": (_i, [_vp, _vp, _u64, _i, _i, _vp]),
+    "gp_calib_p2p_copy_ex": (_i, [_vp, _vp, _u64, _i, _i, _u64, _vp, _vp, _vp]),
     "gp_calib_pingpong": (_i, [_vp, _vp, _i, _i, _u64, _vp, _vp]),
     "gp_last_error_string": (ctypes.c_char_p, []),
     "gp_version": (_i, []),

@@ -18,11 +18,46 @@ constexpr int kCT = 512;
 constexpr int kCU = 8;
 
 // Each warp streams 16-byte vectors, kCU in flight per lane.
+// mode bit 0: pull (remote load, local store) instead of push.
+// mode bit 1: each warp copies contiguous `chunk`-vector pieces taken from a
+//             global counter (the ring kernel's access pattern) instead of
+//             the grid-interleaved stride; bit 2: st.release.sys a flag after
+//             every piece (the ring's publish).
 __global__ void __launch_bounds__(kCT) p2p_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                                       uint64_t nvec, int pull) {
+                                                       uint64_t nvec, int mode, uint64_t chunk,
+                                                       unsigned long long* counter, uint64_t* flags) {
+  const int pull = mode & 1;
   const uint64_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)kCT + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)kCT) >> 5;
+  if (mode & 2) {
+    for (;;) {
+      uint64_t c = 0;
+      if (lane == 0) c = atomicAdd(counter, 1ull);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      const uint64_t b0 = c * chunk;
+      if (b0 >= nvec) break;
+      const uint64_t e0 = min(nvec, b0 + chunk);
+      for (uint64_t base = b0; base < e0; base += 32 * kCU) {
+        uint4 v[kCU];
+#pragma unroll
+        for (int u = 0; u < kCU; ++u) {
+          const uint64_t i = base + u * 32 + lane;
+          if (i < e0) v[u] = pull ? __ldcg(src + i) : __ldg(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kCU; ++u) {
+          const uint64_t i = base + u * 32 + lane;
+          if (i < e0) __stcg(dst + i, v[u]);
+        }
+      }
+      if (mode & 4) {
+        __syncwarp();
+        if (lane == 0) st_release_sys(flags + c, 1);
+      }
+    }
+    return;
+  }
   for (uint64_t base = warp * 32 * kCU; base < nvec; base += nwarps * 32 * kCU) {
     uint4 v[kCU];
 #pragma unroll
@@ -64,13 +99,23 @@ __global__ void pingpong_kernel(uint64_t* mine, uint64_t* theirs, int iters, int
 extern "C" {
 
 int gp_calib_p2p_copy(void* dst, const void* src, uint64_t bytes, int ctas, int pull, void* stream) {
+  return gp_calib_p2p_copy_ex(dst, src, bytes, ctas, pull, 0, nullptr, nullptr, stream);
+}
+
+int gp_calib_p2p_copy_ex(void* dst, const void* src, uint64_t bytes, int ctas, int mode, uint64_t chunk_bytes,
+                         void* counter, void* flags, void* stream) {
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15u) {
     gp_set_error_string("p2p copy needs 16-byte aligned pointers and size");
     return GP_ERR_ARG;
   }
   if (ctas <= 0) ctas = 148;
+  if ((mode & 2) && (!counter || chunk_bytes < 16 || ((mode & 4) && !flags))) {
+    gp_set_error_string("chunked p2p copy needs a counter, chunk size and (mode 4) flags");
+    return GP_ERR_ARG;
+  }
   p2p_copy_kernel<<<ctas, kCT, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<uint4*>(dst), static_cast<const uint4*>(src), bytes / 16, pull);
+      static_cast<uint4*>(dst), static_cast<const uint4*>(src), bytes / 16, mode, chunk_bytes / 16,
+      static_cast<unsigned long long*>(counter), static_cast<uint64_t*>(flags));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gp_set_error_string(std::string("p2p copy launch: ") + cudaGetErrorString(e));

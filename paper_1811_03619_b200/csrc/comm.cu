@@ -115,17 +115,27 @@ void account(gp_stats& s, int rank, int p, uint64_t n, int codec) {
   }
 }
 
-uint32_t pick_chunk(uint64_t n, int p, int G) {
-  static const uint64_t max_chunk = [] {
-    const char* e = std::getenv("PIPESGD_MAX_CHUNK");
-    const uint64_t v = e ? std::strtoull(e, nullptr, 10) : kMaxChunk;
-    return std::max<uint64_t>(kMinChunk, v / kMinChunk * kMinChunk);
-  }();
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
+// Chunk size (elements) for one call: the block split over all warp workers,
+// at least 1024 elements and at most 64 KiB of payload. A chunk is the unit
+// of one system-scope release; measured on 2xB200 (profiles/), more parallel
+// chunks beat fewer releases below 64 MB, and at 64 KiB per release the fence
+// costs ~2% (tools/p2p_pattern_probe.py). Dynamic scheduling evens out the rest.
+uint32_t pick_chunk(uint64_t n, int p, int G, int codec) {
+  static const uint64_t min_bytes = env_u64("PIPESGD_MIN_CHUNK_BYTES", 0);
+  static const uint64_t max_bytes = env_u64("PIPESGD_MAX_CHUNK_BYTES", 65536);
+  static const uint64_t per_warp = std::max<uint64_t>(1, env_u64("PIPESGD_CHUNKS_PER_WARP", 1));
+  const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
+  const uint64_t lo = std::max<uint64_t>(kMinChunk, round_up(min_bytes / w, kMinChunk));
+  const uint64_t hi = std::max<uint64_t>(lo, round_up(max_bytes / w, kMinChunk));
   const uint64_t maxblk = (n + p - 1) / p + 16;
-  const uint64_t workers = (uint64_t)G * kRingWarps;
-  uint64_t ch = round_up((maxblk + workers - 1) / workers, kMinChunk);
-  ch = std::max<uint64_t>(kMinChunk, std::min<uint64_t>(max_chunk, ch));
-  return (uint32_t)ch;
+  const uint64_t workers = (uint64_t)G * kRingWarps * per_warp;
+  const uint64_t ch = round_up((maxblk + workers - 1) / workers, kMinChunk);
+  return (uint32_t)std::max(lo, std::min(hi, ch));
 }
 
 int check_common(gp_comm* c, uint64_t n, int codec) {
@@ -310,7 +320,7 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint6
   P.G = c->G;
   ++c->seq;  // host-side count (info only); the kernel numbers calls on the device
   P.iteration = iteration;
-  P.chunk = pick_chunk(n, p, c->G);
+  P.chunk = pick_chunk(n, p, c->G, codec);
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;
   for (int i = 0; i < c->nlocal; ++i) {

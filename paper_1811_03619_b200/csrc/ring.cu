@@ -83,45 +83,54 @@ __device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
   return *(volatile unsigned long long*)&ctl->abort >= s_seq;
 }
 
-// Lane 0 spins until *f >= seq. Returns false on timeout or abort. Polls
-// with relaxed loads and a short exponential back-off (thousands of warps
-// poll at once; acquire loads in a tight loop would flood L2), then takes
-// the acquire with one final ld.acquire.
-__device__ bool spin_flag(const uint64_t* f, const RingParams& P, const RankCtx& R, Ctl* ctl,
-                          ErrWord* err, int phase, int step, int block) {
-  if (ld_acquire_sys(f) >= s_seq) return true;
+// Flag word: (call sequence << 32) | quant8 scale bits. Carrying the scale in
+// the flag means no chunk has to read (or write) a shared header line.
+__device__ __forceinline__ uint64_t flag_word(float scale) {
+  return ((uint64_t)s_seq << 32) | __float_as_uint(scale);
+}
+
+// Lane 0 spins until the flag carries this call's sequence. Returns the
+// flag word (0 on timeout or abort). Polls with relaxed loads and a short
+// exponential back-off (thousands of warps poll at once; acquire loads in a
+// tight loop would flood L2), then takes the acquire with one ld.acquire.
+__device__ uint64_t spin_flag(const uint64_t* f, const RingParams& P, const RankCtx& R, Ctl* ctl,
+                              ErrWord* err, int phase, int step, int block) {
+  const uint64_t want = (uint64_t)s_seq << 32;
+  uint64_t v = ld_acquire_sys(f);
+  if (v >= want) return v;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
   for (uint32_t it = 1;; ++it) {
-    if (ld_relaxed_sys(f) >= s_seq) {
-      (void)ld_acquire_sys(f);
-      return true;
-    }
+    if (ld_relaxed_sys(f) >= want) return ld_acquire_sys(f);
     __nanosleep(ns);
     if (ns < 256) ns <<= 1;
     if ((it & 63u) == 0) {
       if (aborted(P, ctl)) {
         latch_error(err, kErrTimeout, phase, step, block, R.rank, 1 /* peer aborted */);
-        return false;
+        return 0;
       }
       if (globaltimer() - t0 > P.timeout_ns) {
         latch_error(err, kErrTimeout, phase, step, block, R.rank, 0);
         broadcast_abort(P, R);
-        return false;
+        return 0;
       }
     }
   }
 }
 
-// Warp: wait for (slot, chunk) of this rank's inbox, validate the slot
-// header like collective.py:_expect (:52-64, :109-114), fetch the scale.
+// Warp: wait for (slot, chunk) of this rank's inbox and take the scale from
+// the flag word. With chunk 0 the slot header is validated like
+// collective.py:_expect (:52-64, :109-114): block index, iteration tag and
+// length must be what this rank expects.
 __device__ bool warp_await(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err, int slot,
                            uint32_t c, int phase, int step, int block, uint64_t len, float& scale) {
   int ok = 1;
-  float s = 0.f;
+  uint32_t sb = 0;
   if (lane_id() == 0) {
-    ok = spin_flag(flag_ptr(R.inbox, P.L, slot, c), P, R, ctl, err, phase, step, block);
-    if (ok) {
+    const uint64_t v = spin_flag(flag_ptr(R.inbox, P.L, slot, c), P, R, ctl, err, phase, step, block);
+    ok = v != 0;
+    sb = (uint32_t)v;
+    if (ok && c == 0) {
       const SlotHdr* h = hdr_ptr(R.inbox, P.L, slot);
       const uint32_t hb = __ldcg(&h->block), hi = __ldcg(&h->iteration), hn = __ldcg(&h->n_elems);
       if (hb != (uint32_t)block || hi != P.iteration || hn != (uint32_t)len) {
@@ -129,12 +138,11 @@ __device__ bool warp_await(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrW
         broadcast_abort(P, R);
         ok = 0;
       }
-      s = __ldcg(&h->scale);
     }
   }
   __syncwarp();
   ok = __shfl_sync(0xffffffffu, ok, 0);
-  scale = __shfl_sync(0xffffffffu, s, 0);
+  scale = __uint_as_float(__shfl_sync(0xffffffffu, sb, 0));
   return ok;
 }
 
@@ -148,14 +156,14 @@ __device__ __forceinline__ void write_hdr(const RingParams& P, uint8_t* dst, int
   h->scale = scale;
 }
 
-// Warp: after this warp's payload stores to `dst`, publish the slot header
-// and release the chunk flag at system scope.
+// Warp: after this warp's payload stores to `dst`, release the chunk flag
+// at system scope (chunk 0 also carries the slot header).
 __device__ __forceinline__ void warp_publish(const RingParams& P, uint8_t* dst, int slot, uint32_t c,
                                              int block, uint64_t len, float scale) {
   __syncwarp();
   if (lane_id() == 0) {
-    write_hdr(P, dst, slot, block, len, scale);
-    st_release_sys(flag_ptr(dst, P.L, slot, c), s_seq);  // release: orders the warp's stores
+    if (c == 0) write_hdr(P, dst, slot, block, len, scale);
+    st_release_sys(flag_ptr(dst, P.L, slot, c), flag_word(scale));  // release: orders the warp's stores
   }
 }
 
@@ -164,10 +172,11 @@ __device__ __forceinline__ void warp_publish_all(const RingParams& P, const Rank
                                                  uint64_t len, float scale) {
   __syncwarp();
   if (lane_id() == 0) {
-    for (int d = 1; d < P.p; ++d) write_hdr(P, R.peer[(R.rank + d) % P.p], ag_slot(P.p, b), b, len, scale);
-    fence_sys();  // one system fence, then relaxed-cost releases to every peer
+    if (c == 0)
+      for (int d = 1; d < P.p; ++d) write_hdr(P, R.peer[(R.rank + d) % P.p], ag_slot(P.p, b), b, len, scale);
+    fence_sys();  // one system fence, then relaxed flag stores to every peer
     for (int d = 1; d < P.p; ++d)
-      st_release_sys(flag_ptr(R.peer[(R.rank + d) % P.p], P.L, ag_slot(P.p, b), c), s_seq);
+      st_relaxed_sys(flag_ptr(R.peer[(R.rank + d) % P.p], P.L, ag_slot(P.p, b), c), flag_word(scale));
   }
 }
 
@@ -237,6 +246,19 @@ __device__ __forceinline__ void stamp(const RingParams& P, uint32_t wid, int lra
     P.trace[((uint64_t)lrank * P.G * kWarps + wid) * kTraceSlots + k] = globaltimer();
 }
 
+// Dynamic chunk scheduling: the warps of one rank take chunk indices of a
+// phase from a counter in the rank's control block (reset when the call
+// closes). Flags are per chunk, not per warp, so ranks need not agree on
+// which warp handles which chunk; fast warps take more chunks, which evens
+// out the unequal NVLink shares warps get under arbitration.
+// Phases: 0 quant8 step-0 max, 1 step-0 send, 2+2s fold of step s,
+// 3+2s quant8 push of step s, 20+k allgather of the k-th block.
+__device__ __forceinline__ uint32_t grab(Ctl* ctl, int phase) {
+  uint32_t c = 0;
+  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&ctl->next[phase], 1ull);
+  return __shfl_sync(0xffffffffu, c, 0);
+}
+
 template <int E>
 struct XIn {
   FV<E> x;
@@ -250,7 +272,6 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   constexpr int E = CodecT<C>::E;
   const int G = P.G;
   const int lr = blockIdx.x / G;
-  const uint32_t W = (uint32_t)G * kWarps;
   const uint32_t wid = (blockIdx.x % G) * kWarps + (threadIdx.x >> 5);
   const RankCtx& R = P.rk[lr];
   const int p = P.p, r = R.rank, succ = (r + 1) % p;
@@ -267,7 +288,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     Q8 q = q8_make(0.f);
     if constexpr (C == kQuant8) {
       uint32_t m = 0;
-      for (uint32_t c = wid; c < B.nch; c += W)
+      for (uint32_t c = grab(ctl, 0); c < B.nch; c = grab(ctl, 0))
         for_groups<C>(P, B, c,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                       [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
@@ -276,7 +297,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       q = q8_make(q8_scale(vmax));
     }
     uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
-    for (uint32_t c = wid; c < B.nch; c += W) {
+    for (uint32_t c = grab(ctl, 1); c < B.nch; c = grab(ctl, 1)) {
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
@@ -311,10 +332,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
 
     if constexpr (C != kQuant8) {
       const Q8 q = q8_make(0.f);
-      for (uint32_t c = wid; c < B.nch; c += W) {
+      bool first = true;
+      for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
         float sin;
         if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
-        if (c == wid) stamp(P, wid, lr, 2 + 2 * s);
+        if (first) stamp(P, wid, lr, 2 + 2 * s);
+        first = false;
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                         emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(v.x, decode_v<C>(v.in, sin)), q, bad), 0.f);
@@ -325,10 +348,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     } else {
       // pass A: fold into `out` (scratch for this block) and reduce the max
       uint32_t m = 0;
-      for (uint32_t c = wid; c < B.nch; c += W) {
+      bool first = true;
+      for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
         float sin;
         if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
-        if (c == wid) stamp(P, wid, lr, 2 + 2 * s);
+        if (first) stamp(P, wid, lr, 2 + 2 * s);
+        first = false;
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
                         const FV<E> acc = add_v(v.x, decode_v<C>(v.in, sin));
@@ -339,8 +364,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       float vmax;
       if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
       const Q8 q = q8_make(q8_scale(vmax));
-      // pass B: encode the partial with the block scale and push it
-      for (uint32_t c = wid; c < B.nch; c += W) {
+      // pass B: encode the partial with the block scale and push it (any
+      // warp may take any chunk: pass A's partials are visible GPU-wide
+      // after the barrier and are read through L2)
+      for (uint32_t c = grab(ctl, 3 + 2 * s); c < B.nch; c = grab(ctl, 3 + 2 * s)) {
         for_groups<C>(P, B, c,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
                         return load_fv<E, false>(out, g0, lo, hi);
@@ -364,10 +391,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const Blk B = get_blk(P, b);
     const int step = (r - b + p) % p;  // reference allgather step that delivers block b
     const uint8_t* in_slot = slot_ptr(R.inbox, P.L, ag_slot(p, b));
-    for (uint32_t c = wid; c < B.nch; c += W) {
+    bool first = true;
+    for (uint32_t c = grab(ctl, 20 + k); c < B.nch; c = grab(ctl, 20 + k)) {
       float sin;
       if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) return;
-      if (k == 1 && c == wid) stamp(P, wid, lr, 18);
+      if (k == 1 && first) stamp(P, wid, lr, 18);
+      first = false;
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
                       return load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
@@ -395,6 +424,7 @@ __global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __gr
     if (prev == (unsigned long long)P.G * kWarps - 1) {
       ctl->exits = 0;
       ctl->bar = 0;
+      for (int i = 0; i < 32; ++i) ctl->next[i] = 0;
       __threadfence();
       atomicExch(&ctl->calls, (unsigned long long)s_seq);
     }

@@ -9,7 +9,7 @@ namespace gp {
 constexpr int kRingThreads = 512;
 constexpr int kRingWarps = kRingThreads / 32;
 constexpr uint32_t kMinChunk = 1024;   // elements per warp chunk; flags are sized for this
-constexpr uint32_t kMaxChunk = 4096;   // default largest warp chunk (16 KiB of fp32)
+constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of fp32)
 
 // Per-rank inbox layout (identical on every rank of a communicator). Peers
 // write payload, headers and flags here over NVLink; ctl/err are private.
@@ -27,6 +27,7 @@ struct Ctl {                   // rank-private control block
   unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier
   unsigned long long calls;    // completed calls; this call's sequence number is calls + 1
   unsigned long long exits;    // warps that finished the current call
+  unsigned long long next[32]; // per-phase chunk counters (dynamic chunk scheduling)
 };
 
 struct SlotHdr {               // written by the sender before each chunk flag
