@@ -154,7 +154,7 @@ def encode_async(x: torch.Tensor, codec: Codec, payload: torch.Tensor, status: C
                  stream: int | None = None) -> None:
     """Stream-ordered encode of x into payload; scale lands in status."""
     s = _stream_ptr(x.device) if stream is None else stream
-    _lib.call("gp_encode", int(codec), x.data_ptr(), x.numel(), payload.data_ptr(), status.ptr, s)
+    _lib.call("gp_encode", int(as_codec(codec)), x.data_ptr(), x.numel(), payload.data_ptr(), status.ptr, s)
 
 
 def compress(vec, codec: Codec) -> CompressedBlock:
@@ -188,7 +188,7 @@ def roundtrip_async(x: torch.Tensor, codec: Codec, out: torch.Tensor, status: Co
                     stream: int | None = None) -> torch.Tensor:
     """out = D(C(x)) in one pass (two for quant8), no payload materialised."""
     s = _stream_ptr(x.device) if stream is None else stream
-    _lib.call("gp_roundtrip", int(codec), x.data_ptr(), out.data_ptr(), x.numel(), status.ptr, s)
+    _lib.call("gp_roundtrip", int(as_codec(codec)), x.data_ptr(), out.data_ptr(), x.numel(), status.ptr, s)
     return out
 
 

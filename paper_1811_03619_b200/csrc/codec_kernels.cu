@@ -23,6 +23,7 @@ void gp_set_error_string(const std::string& m);  // comm.cu: the thread's last e
 namespace {
 
 constexpr int kT = 256;
+constexpr int kU = 4;  // groups per thread per streaming iteration
 
 int cfail(int code, const std::string& m);
 
@@ -35,7 +36,7 @@ uint32_t grid_for(uint64_t n) {
     if (sms <= 0) sms = 148;
   }
   const uint64_t groups = (n + 3) / 4;
-  const uint64_t want = (groups + kT - 1) / kT;
+  const uint64_t want = (groups + kT * kU - 1) / (kT * kU);
   const uint64_t cap = (uint64_t)sms * 8;
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
@@ -43,6 +44,24 @@ uint32_t grid_for(uint64_t n) {
 #define GROUP_LOOP(E) \
   for (uint64_t g0 = (uint64_t)(E) * (blockIdx.x * (uint64_t)kT + threadIdx.x); g0 < n; \
        g0 += (uint64_t)(E) * kT * gridDim.x)
+
+// Streaming loop with kU groups per thread per iteration: every load of an
+// iteration is issued before its first store (more bytes in flight per
+// thread for these short HBM-bound kernels).
+template <int E, typename L, typename S>
+__device__ __forceinline__ void stream_groups(uint64_t n, L&& load, S&& use) {
+  const uint64_t stride = (uint64_t)E * kT * gridDim.x;
+  for (uint64_t base = (uint64_t)E * (blockIdx.x * (uint64_t)kT + threadIdx.x); base < n; base += stride * kU) {
+    using T = decltype(load(base));
+    T v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (base + u * stride < n) v[u] = load(base + u * stride);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (base + u * stride < n) use(base + u * stride, v[u]);
+  }
+}
 
 __global__ void __launch_bounds__(kT) absmax_kernel(const float* __restrict__ x, uint64_t n,
                                                     gp_codec_status* st) {
@@ -77,10 +96,10 @@ __global__ void __launch_bounds__(kT) encode_kernel(const float* __restrict__ x,
   constexpr int E = CodecT<C>::E;
   const Q8 q = status_scale<C>(st);
   int bad = 0;
-  GROUP_LOOP(E) {
-    const uint4 pk = encode_v<C>(load_fv<E>(x, g0, 0, n), q, bad);
-    store_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0), pk);
-  }
+  stream_groups<E>(n, [&](uint64_t g0) { return load_fv<E>(x, g0, 0, n); },
+                   [&](uint64_t g0, const FV<E>& v) {
+                     store_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0), encode_v<C>(v, q, bad));
+                   });
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
 
@@ -89,9 +108,8 @@ __global__ void __launch_bounds__(kT) decode_kernel(const uint8_t* payload, cons
                                                     float* out) {
   constexpr int E = CodecT<C>::E;
   const float s = (C == kQuant8) ? *scale : 0.f;
-  GROUP_LOOP(E) {
-    store_fv<E>(out, g0, 0, n, decode_v<C>(load_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0)), s));
-  }
+  stream_groups<E>(n, [&](uint64_t g0) { return load_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0)); },
+                   [&](uint64_t g0, const uint4& v) { store_fv<E>(out, g0, 0, n, decode_v<C>(v, s)); });
 }
 
 template <int C>
@@ -100,10 +118,10 @@ __global__ void __launch_bounds__(kT) roundtrip_kernel(const float* __restrict__
   constexpr int E = CodecT<C>::E;
   const Q8 q = status_scale<C>(st);
   int bad = 0;
-  GROUP_LOOP(E) {
-    const uint4 pk = encode_v<C>(load_fv<E>(x, g0, 0, n), q, bad);
-    store_fv<E>(out, g0, 0, n, decode_v<C>(pk, q.s));
-  }
+  stream_groups<E>(n, [&](uint64_t g0) { return load_fv<E>(x, g0, 0, n); },
+                   [&](uint64_t g0, const FV<E>& v) {
+                     store_fv<E>(out, g0, 0, n, decode_v<C>(encode_v<C>(v, q, bad), q.s));
+                   });
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
 
@@ -113,16 +131,24 @@ __global__ void __launch_bounds__(kT) consume_update_kernel(float* w, const uint
   constexpr int E = CodecT<C>::E;
   const float s = (C == kQuant8) ? *scale : 0.f;
   const float fp = (float)p;
-  GROUP_LOOP(E) {
-    const FV<E> g = decode_v<C>(load_pay<C>(slot, g0, 0, (int)(min(n, g0 + E) - g0)), s);
-    FV<E> v = load_fv<E, false>(w, g0, 0, n);
+  struct WG {
+    FV<E> w;
+    uint4 g;
+  };
+  stream_groups<E>(n,
+                   [&](uint64_t g0) {
+                     return WG{load_fv<E, false>(w, g0, 0, n), load_pay<C>(slot, g0, 0, (int)(min(n, g0 + E) - g0))};
+                   },
+                   [&](uint64_t g0, const WG& in) {
+                     const FV<E> g = decode_v<C>(in.g, s);
+                     FV<E> v = in.w;
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const float gm = p == 1 ? g.v[i] : __fdiv_rn(g.v[i], fp);
-      v.v[i] = __fsub_rn(v.v[i], __fmul_rn(lr, gm));
-    }
-    store_fv<E>(w, g0, 0, n, v);
-  }
+                     for (int i = 0; i < E; ++i) {
+                       const float gm = p == 1 ? g.v[i] : __fdiv_rn(g.v[i], fp);
+                       v.v[i] = __fsub_rn(v.v[i], __fmul_rn(lr, gm));
+                     }
+                     store_fv<E>(w, g0, 0, n, v);
+                   });
 }
 
 int cfail(int code, const std::string& m) {

@@ -84,6 +84,8 @@ int alloc_inbox(gp_comm* c, int i) {
   // Flags, headers, ctl and error word must start at zero; payload need not.
   e = cudaMemset(c->inbox[i], 0, c->L.off_payload);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(inbox)");
+  e = cudaMemset(c->inbox[i] + c->L.off_err, 0xFF, sizeof(unsigned long long));  // no error
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(error word)");
   return GP_OK;
 }
 
@@ -368,18 +370,26 @@ int gp_comm_poll_error(gp_comm* c, gp_error* out) {
   if (!c || !out) return fail(GP_ERR_ARG, "null argument");
   DeviceGuard g(c->device);
   std::memset(out, 0, sizeof(*out));
+  unsigned long long best = ~0ull;
   for (int i = 0; i < c->nlocal; ++i) {
     ErrWord w;
     cudaError_t e = cudaMemcpy(&w, c->inbox[i] + c->L.off_err, sizeof(w), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(error word)");
-    if (w.kind != 0) {
-      if (out->kind == 0) {
-        out->kind = w.kind; out->phase = w.phase; out->step = w.step;
-        out->block = w.block; out->rank = w.rank; out->detail = w.detail;
-      }
-      e = cudaMemset(c->inbox[i] + c->L.off_err, 0, sizeof(ErrWord));
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(error word)");
+    if (w.code != ~0ull) {
+      best = std::min(best, w.code);
+      const unsigned long long none = ~0ull;
+      e = cudaMemcpy(c->inbox[i] + c->L.off_err, &none, sizeof(none), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(reset error word)");
     }
+  }
+  if (best != ~0ull) {
+    static const int phases[4] = {kPhRS, kPhBarrier, kPhAG, kPhLocal};
+    out->phase = phases[(best >> 60) & 0xF];
+    out->step = (int)((best >> 52) & 0xFF);
+    out->kind = (int)((best >> 48) & 0xF);
+    out->block = (int)((best >> 40) & 0xFF) - 1;
+    out->rank = (int)((best >> 32) & 0xFF);
+    out->detail = (int)(uint32_t)best;
   }
   return GP_OK;
 }

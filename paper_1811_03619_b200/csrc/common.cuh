@@ -20,15 +20,19 @@ enum Codec : int { kNone = 0, kTrunc16 = 1, kQuant8 = 2 };
 enum ErrKind : int { kErrNone = 0, kErrNonFinite = 1, kErrTimeout = 2, kErrHeader = 3 };
 enum Phase : int { kPhRS = 0, kPhAG = 1, kPhBarrier = 2, kPhLocal = 3 };
 
+// Device error word: one u64 so the EARLIEST failure wins via atomicMin,
+// ordered by (phase order, step) like the reference, which fails at the
+// first step that cannot complete. 0 = no error.
+//   [63:60] phase order (0 reduce-scatter, 1 barrier, 2 allgather, 3 local)
+//   [59:52] step   [51:48] kind   [47:40] block+1   [39:32] rank   [31:0] detail
 struct ErrWord {
-  int kind;
-  int phase;
-  int step;
-  int block;
-  int rank;
-  int detail;
-  int pad[2];
+  unsigned long long code;
+  unsigned long long pad[3];
 };
+
+__host__ __device__ inline int phase_order(int phase) {
+  return phase == kPhRS ? 0 : phase == kPhBarrier ? 1 : phase == kPhAG ? 2 : 3;
+}
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
@@ -58,17 +62,15 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// Record the first error only (later ones are consequences).
+// Record a failure; the earliest (phase, step) is kept.
 __device__ __forceinline__ void latch_error(ErrWord* e, int kind, int phase, int step, int block,
                                             int rank, int detail) {
-  if (atomicCAS(&e->kind, 0, kind) == 0) {
-    e->phase = phase;
-    e->step = step;
-    e->block = block;
-    e->rank = rank;
-    e->detail = detail;
-    __threadfence();
-  }
+  const unsigned long long code =
+      ((unsigned long long)(phase_order(phase) & 0xF) << 60) | ((unsigned long long)(step & 0xFF) << 52) |
+      ((unsigned long long)(kind & 0xF) << 48) | ((unsigned long long)((block + 1) & 0xFF) << 40) |
+      ((unsigned long long)(rank & 0xFF) << 32) | (unsigned long long)(uint32_t)detail;
+  atomicMin(&e->code, code);
+  __threadfence();
 }
 
 __device__ __forceinline__ bool nonfinite(float x) {

@@ -199,7 +199,13 @@ class RankEngine:
             self.summed = torch.empty(self.n, dtype=torch.float32, device=self.dev)
             self.slots = [_Slot(config.codec, torch.zeros(self.n * w, dtype=torch.uint8, device=self.dev),
                                 CodecStatus(self.dev)) for _ in range(K)]
-            self.sync_slot = _Slot(Codec.NONE, self.summed.view(torch.uint8), CodecStatus(self.dev))
+            # d_sync consumes the raw fp32 sum; at p=1 the reference's ring is an
+            # identity copy (collective.py:153-154), so the local buffer is the sum
+            if world == 1:
+                self.sync_slots = [_Slot(Codec.NONE, self.local[i].view(torch.uint8), CodecStatus(self.dev))
+                                   for i in range(K)]
+            else:
+                self.sync_slots = [_Slot(Codec.NONE, self.summed.view(torch.uint8), CodecStatus(self.dev))] * K
             self.local_status = [CodecStatus(self.dev) for _ in range(K)]
             self.slot_nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
             self.losses = torch.zeros(config.iterations + 2, dtype=torch.float32, device=self.dev)
@@ -266,18 +272,23 @@ class RankEngine:
         i = t % self.K
         self.ms.wait_event(self.ev_local[i])
         e0 = self._ev(self.ms) if self.tracing else None
-        allreduce_into(self.local[i], self.summed, self.ep, self.cfg.codec, t, self.ms)
+        if self.world > 1:
+            allreduce_into(self.local[i], self.summed, self.ep, self.cfg.codec, t, self.ms)
+            src = self.summed
+        else:
+            src = self.local[i]  # p == 1: the ring is the identity (no codec, no copy)
         e1 = self._ev(self.ms) if self.tracing else None
         if requant:
             slot = self.slots[i]
-            encode_async(self.summed, self.cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
+            encode_async(src, self.cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
         else:
-            slot = self.sync_slot
+            slot = self.sync_slots[i]
         ready = torch.cuda.Event(enable_timing=self.tracing)
         ready.record(self.ms)
         if self.tracing:
             self._rec(t, STAGE_ALLREDUCE, e0, ready)
-            self._rec(t, "ring", e0, e1)
+            if self.world > 1:
+                self._rec(t, "ring", e0, e1)
             if requant:
                 self._rec(t, "recompress", e1, ready)
         self.buffer.put(t, slot, ready)
