@@ -10,6 +10,8 @@
  * (/root/reference/pkg/src/gradpipe):
  *   gp_allreduce            collective.py:143-163 ring_allreduce
  *                           collective.py:166-212 pipelined_allreduce (same bits)
+ *   gp_allreduce_ex         the ring fused with the engine's local pre-compress
+ *                           (engine.py:333) and pipe re-compress of the sum (engine.py:407)
  *   gp_allreduce_emulated   the same ring with all p ranks on one device
  *                           (collective.py:77-139 driven like tests/helpers.py:10-29)
  *   gp_comm_create/connect  transport.py:150-177 InProcTransport(world).endpoint(r)
@@ -96,6 +98,19 @@ int gp_allreduce(gp_comm* comm, const float* in, float* out, uint64_t n, int cod
                  uint32_t iteration, void* stream);
 int gp_allreduce_emulated(gp_comm* comm, const float* const* ins, float* const* outs, uint64_t n,
                           int codec, uint32_t iteration, void* stream);
+/* Fused variants. flags:
+ *   GP_RING_PRECOMPRESS: `in` is the raw local gradient; the ring applies the
+ *     engine's whole-vector D(C(.)) (engine.py:333, :355/:400) while loading it.
+ *   GP_RING_SLOT_OUT: instead of the fp32 sum, write C(sum) with the whole-vector
+ *     codec (engine.py:407) to `slot` (n * width bytes) and its scale to `slot_scale`
+ *     (device f32); `out` is then scratch (quant8) and its contents undefined.
+ * Results are bit-identical to ring_allreduce followed by compress/decompress. */
+enum { GP_RING_PRECOMPRESS = 1, GP_RING_SLOT_OUT = 2 };
+int gp_allreduce_ex(gp_comm* comm, const float* in, float* out, void* slot, float* slot_scale, uint64_t n,
+                    int codec, int flags, uint32_t iteration, void* stream);
+int gp_allreduce_emulated_ex(gp_comm* comm, const float* const* ins, float* const* outs, void* const* slots,
+                             float* const* slot_scales, uint64_t n, int codec, int flags, uint32_t iteration,
+                             void* stream);
 int gp_comm_poll_error(gp_comm* comm, gp_error* out); /* call after the stream completed; clears */
 int gp_get_stats(gp_comm* comm, int rank, gp_stats* out);
 int gp_reset_stats(gp_comm* comm);

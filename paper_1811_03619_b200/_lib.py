@@ -19,12 +19,14 @@ LIB_PATH = os.environ.get("PIPESGD_LIB") or os.path.join(HERE, "libpipesgd.so")
 GP_OK = 0
 GP_FAIL_NONFINITE, GP_FAIL_TIMEOUT, GP_FAIL_HEADER = 1, 2, 3
 GP_PHASE_RS, GP_PHASE_AG, GP_PHASE_BARRIER = 0, 1, 2
+GP_RING_PRECOMPRESS, GP_RING_SLOT_OUT = 1, 2
 
 # Every symbol include/pipesgd.h declares (checked by tests/test_cabi.py).
 EXPORTS = (
     "gp_comm_create", "gp_comm_create_emulated", "gp_comm_ipc_handle", "gp_comm_connect_ipc",
     "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_info", "gp_comm_destroy",
-    "gp_allreduce", "gp_allreduce_emulated", "gp_comm_poll_error", "gp_get_stats",
+    "gp_allreduce", "gp_allreduce_ex", "gp_allreduce_emulated", "gp_allreduce_emulated_ex",
+    "gp_comm_poll_error", "gp_get_stats",
     "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update",
     "gp_calib_p2p_copy", "gp_calib_p2p_copy_ex", "gp_calib_pingpong", "gp_last_error_string", "gp_version",
 )
@@ -55,6 +57,9 @@ _SIGS = {
     "gp_comm_destroy": (_i, [_vp]),
     "gp_allreduce": (_i, [_vp, _vp, _vp, _u64, _i, _u32, _vp]),
     "gp_allreduce_emulated": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _u64, _i, _u32, _vp]),
+    "gp_allreduce_ex": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _i, _i, _u32, _vp]),
+    "gp_allreduce_emulated_ex": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                      ctypes.POINTER(_vp), _u64, _i, _i, _u32, _vp]),
     "gp_comm_poll_error": (_i, [_vp, ctypes.POINTER(GpError)]),
     "gp_get_stats": (_i, [_vp, _i, ctypes.POINTER(GpStats)]),
     "gp_reset_stats": (_i, [_vp]),

@@ -19,6 +19,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _lib
 from .compression import Codec, as_codec
 from .errors import CollectiveError
 from .transport import GpuEndpoint
@@ -58,13 +59,21 @@ def _device_input(local, device: torch.device) -> torch.Tensor:
     return t
 
 
-def allreduce_into(x: torch.Tensor, out: torch.Tensor, endpoint: GpuEndpoint, codec=Codec.NONE,
-                   iteration: int = 0, stream: torch.cuda.Stream | None = None) -> None:
+def allreduce_into(x: torch.Tensor, out: torch.Tensor | None, endpoint: GpuEndpoint, codec=Codec.NONE,
+                   iteration: int = 0, stream: torch.cuda.Stream | None = None, precompress: bool = False,
+                   slot: torch.Tensor | None = None, slot_scale: torch.Tensor | None = None) -> None:
     """Stream-ordered, non-blocking form used by the pipelined engine:
     enqueue the fused ring on `stream` (default: current stream of the
-    endpoint's device). Errors surface at `endpoint_wait`."""
+    endpoint's device). Errors surface at `endpoint_wait`.
+
+    precompress=True: x is the raw local gradient; the ring applies the
+      engine's whole-vector D(C(x)) while loading it (engine.py:333).
+    slot=...: write C(sum) (whole-vector codec, engine.py:407) into the uint8
+      `slot` and its scale into `slot_scale` instead of the fp32 sum; `out`
+      is then scratch (needed for quant8 at p > 1)."""
     s = stream if stream is not None else torch.cuda.current_stream(endpoint.device)
-    endpoint._launch(x, out, as_codec(codec), iteration, s)
+    flags = (_lib.GP_RING_PRECOMPRESS if precompress else 0) | (_lib.GP_RING_SLOT_OUT if slot is not None else 0)
+    endpoint._launch(x, out, as_codec(codec), iteration, s, flags, slot, slot_scale)
 
 
 def endpoint_wait(endpoint: GpuEndpoint, n: int, stream: torch.cuda.Stream | None = None) -> None:

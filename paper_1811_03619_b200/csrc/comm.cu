@@ -304,22 +304,52 @@ int gp_comm_destroy(gp_comm* c) {
   return GP_OK;
 }
 
-static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int codec,
-                  uint32_t iteration, cudaStream_t st) {
-  const int p = c->world;
-  if (p == 1) {
+__global__ void status_to_error_kernel(const gp_codec_status* st, ErrWord* e, int rank) {
+  if (st->nonfinite) latch_error(e, kErrNonFinite, kPhRS, 0, rank, rank, 0);
+}
+
+// p == 1: the reference's ring is an identity copy (collective.py:153-154);
+// the fused flags reduce to the whole-vector codec kernels.
+static int launch_single(gp_comm* c, const float* in, float* out, void* slot, float* slot_scale, uint64_t n,
+                         int codec, int flags, cudaStream_t st) {
+  auto* status = reinterpret_cast<gp_codec_status*>(c->inbox[0] + c->L.off_ctl + 2048);
+  auto* errw = reinterpret_cast<ErrWord*>(c->inbox[0] + c->L.off_err);
+  int rc = GP_OK;
+  if (flags & GP_RING_SLOT_OUT) {
+    // C(D(C(x))) == C(x) for every codec (quant8: the scale snaps to itself)
+    rc = gp_encode(codec, in, n, slot, status, st);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(slot_scale, &status->scale, 4, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(slot scale)");
+  } else if (flags & GP_RING_PRECOMPRESS) {
+    rc = gp_roundtrip(codec, in, out, n, status, st);
+    if (rc) return rc;
+  } else {
     if (n) {
-      cudaError_t e = cudaMemcpyAsync(outs[0], ins[0], n * 4, cudaMemcpyDeviceToDevice, st);
+      cudaError_t e = cudaMemcpyAsync(out, in, n * 4, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
     }
     return GP_OK;
   }
+  status_to_error_kernel<<<1, 1, 0, st>>>(status, errw, c->rank);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GP_OK : cuda_fail(e, "status kernel");
+}
+
+static int launch(gp_comm* c, const float* const* ins, float* const* outs, void* const* slots,
+                  float* const* slot_scales, uint64_t n, int codec, int flags, uint32_t iteration,
+                  cudaStream_t st) {
+  const int p = c->world;
+  if (p == 1)
+    return launch_single(c, ins[0], outs[0], slots ? slots[0] : nullptr, slot_scales ? slot_scales[0] : nullptr,
+                         n, codec, flags, st);
   RingParams P{};
   P.L = c->L;
   P.n = n;
   P.p = p;
   P.codec = codec;
   P.G = c->G;
+  P.pre = (flags & GP_RING_PRECOMPRESS) ? 1 : 0;
   ++c->seq;  // host-side count (info only); the kernel numbers calls on the device
   P.iteration = iteration;
   P.chunk = pick_chunk(n, p, c->G, codec);
@@ -329,6 +359,8 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint6
     RankCtx& R = P.rk[i];
     R.x = ins[i];
     R.out = outs[i];
+    R.slot = (flags & GP_RING_SLOT_OUT) ? static_cast<uint8_t*>(slots[i]) : nullptr;
+    R.slot_scale = (flags & GP_RING_SLOT_OUT) ? slot_scales[i] : nullptr;
     R.rank = c->nlocal == 1 ? c->rank : i;
     R.inbox = c->inbox[i];
     for (int q = 0; q < p; ++q) R.peer[q] = c->peer[q];
@@ -340,30 +372,60 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, uint6
   return GP_OK;
 }
 
+static int check_flags(gp_comm* c, int flags, uint64_t n, const float* out, void* slot, float* slot_scale,
+                       int codec) {
+  if (flags & ~(GP_RING_PRECOMPRESS | GP_RING_SLOT_OUT)) return fail(GP_ERR_ARG, "unknown ring flags");
+  if (flags & GP_RING_SLOT_OUT) {
+    if (n && (!slot || !slot_scale)) return fail(GP_ERR_ARG, "slot output needs a payload and a scale");
+    if (n && misaligned(slot)) return fail(GP_ERR_ARG, "slot payload must be 16-byte aligned");
+    if (n && codec == GP_CODEC_QUANT8 && c->world > 1 && !out)
+      return fail(GP_ERR_ARG, "quant8 slot output needs `out` as scratch");
+  } else if (n && !out) {
+    return fail(GP_ERR_ARG, "null output");
+  }
+  return GP_OK;
+}
+
 int gp_allreduce(gp_comm* c, const float* in, float* out, uint64_t n, int codec, uint32_t iteration,
                  void* stream) {
+  return gp_allreduce_ex(c, in, out, nullptr, nullptr, n, codec, 0, iteration, stream);
+}
+
+int gp_allreduce_ex(gp_comm* c, const float* in, float* out, void* slot, float* slot_scale, uint64_t n,
+                    int codec, int flags, uint32_t iteration, void* stream) {
   int rc = check_common(c, n, codec);
   if (rc) return rc;
   if (c->nlocal != 1) return fail(GP_ERR_STATE, "use gp_allreduce_emulated on an emulated communicator");
   if (!c->connected) return fail(GP_ERR_STATE, "communicator is not connected to its peers");
-  if (n && (!in || !out)) return fail(GP_ERR_ARG, "null buffer");
-  if (n && (misaligned(in) || misaligned(out))) return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
-  if (n && in < out + n && out < in + n) return fail(GP_ERR_ARG, "input and output overlap");
+  if ((rc = check_flags(c, flags, n, out, slot, slot_scale, codec))) return rc;
+  if (n && !in) return fail(GP_ERR_ARG, "null buffer");
+  if (n && (misaligned(in) || (out && misaligned(out)))) return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
+  if (n && out && in < out + n && out < in + n) return fail(GP_ERR_ARG, "input and output overlap");
   DeviceGuard g(c->device);
-  return launch(c, &in, &out, n, codec, iteration, static_cast<cudaStream_t>(stream));
+  return launch(c, &in, &out, &slot, &slot_scale, n, codec, flags, iteration, static_cast<cudaStream_t>(stream));
 }
 
 int gp_allreduce_emulated(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int codec,
                           uint32_t iteration, void* stream) {
+  return gp_allreduce_emulated_ex(c, ins, outs, nullptr, nullptr, n, codec, 0, iteration, stream);
+}
+
+int gp_allreduce_emulated_ex(gp_comm* c, const float* const* ins, float* const* outs, void* const* slots,
+                             float* const* slot_scales, uint64_t n, int codec, int flags, uint32_t iteration,
+                             void* stream) {
   int rc = check_common(c, n, codec);
   if (rc) return rc;
   if (c->nlocal == 1 && c->world > 1) return fail(GP_ERR_STATE, "not an emulated communicator");
   for (int i = 0; i < c->nlocal; ++i) {
-    if (n && (!ins[i] || !outs[i])) return fail(GP_ERR_ARG, "null buffer");
-    if (n && (misaligned(ins[i]) || misaligned(outs[i]))) return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
+    if ((rc = check_flags(c, flags, n, outs[i], slots ? slots[i] : nullptr, slot_scales ? slot_scales[i] : nullptr,
+                          codec)))
+      return rc;
+    if (n && !ins[i]) return fail(GP_ERR_ARG, "null buffer");
+    if (n && (misaligned(ins[i]) || (outs[i] && misaligned(outs[i]))))
+      return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
   }
   DeviceGuard g(c->device);
-  return launch(c, ins, outs, n, codec, iteration, static_cast<cudaStream_t>(stream));
+  return launch(c, ins, outs, slots, slot_scales, n, codec, flags, iteration, static_cast<cudaStream_t>(stream));
 }
 
 int gp_comm_poll_error(gp_comm* c, gp_error* out) {

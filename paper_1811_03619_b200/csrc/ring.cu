@@ -265,6 +265,18 @@ struct XIn {
   uint4 in;
 };
 
+// Second max slot of a quant8 barrier (fused pre-compress: the own block's
+// raw max). Each warp atomically maxes it before its barrier arrival, so it
+// is complete once warp_barrier_max returned.
+__device__ __forceinline__ float read_max_slot(Ctl* ctl, int idx) {
+  uint32_t w = 0;
+  if (lane_id() == 0) {
+    const unsigned long long x = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->maxslot[idx]));
+    w = ((uint32_t)(x >> 32) == s_seq) ? (uint32_t)x : 0u;
+  }
+  return __uint_as_float(__shfl_sync(0xffffffffu, w, 0));
+}
+
 }  // namespace
 
 template <int C>
@@ -279,21 +291,72 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   ErrWord* err = reinterpret_cast<ErrWord*>(R.inbox + P.L.off_err);
   const float* __restrict__ x = R.x;
   float* out = R.out;
+  const bool slot_mode = R.slot != nullptr;
   int bad = 0;
   stamp(P, wid, lr, 0);
+
+  // Local pre-compress fused into every load of x (engine.py:333, :355/:400:
+  // the ring input is D(C(grad)) under the whole-vector codec). For quant8
+  // its scale needs max|grad| over the whole vector: one extra read pass.
+  Q8 q0 = q8_make(0.f);
+  auto px = [&](FV<E> v) -> FV<E> {
+    if (P.pre) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
+      if constexpr (C == kTrunc16) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v.v[i] = t16_decode(t16_encode(v.v[i]));
+      } else if constexpr (C == kQuant8) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v.v[i] = q8_decode(q8_encode(v.v[i], q0), q0.s);
+      }
+    }
+    return v;
+  };
 
   // ---- reduce-scatter step 0, send side: C(x_r[block r]) -> succ slot 0
   {
     const Blk B = get_blk(P, r);
     Q8 q = q8_make(0.f);
     if constexpr (C == kQuant8) {
-      uint32_t m = 0;
-      for (uint32_t c = grab(ctl, 0); c < B.nch; c = grab(ctl, 0))
-        for_groups<C>(P, B, c,
-                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
-                      [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
       float vmax;
-      if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
+      if (!P.pre) {
+        uint32_t m = 0;
+        for (uint32_t c = grab(ctl, 0); c < B.nch; c = grab(ctl, 0))
+          for_groups<C>(P, B, c,
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                        [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
+        if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
+      } else {
+        // one pass over the whole local vector: max|x| (pre-compress scale)
+        // and max|x| over the own block, whose D(C(.)) maximum is
+        // D(C(max|x_r|)) because encode/decode are monotone in |x|
+        Blk W;
+        W.start = 0; W.len = P.n; W.A = 0;
+        W.nch = P.n ? (uint32_t)((P.n + P.chunk - 1) / P.chunk) : 0u;
+        uint32_t m = 0, mo = 0;
+        for (uint32_t c = grab(ctl, 0); c < W.nch; c = grab(ctl, 0))
+          for_groups<C>(P, W, c,
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                        [&](uint64_t g0, uint64_t, uint64_t, int, int, const FV<E>& v) {
+                          m = max(m, absmax_bits(v));
+#pragma unroll
+                          for (int i = 0; i < E; ++i) {
+                            const uint64_t g = g0 + i;
+                            if (g >= B.start && g < B.start + B.len) mo = max(mo, __float_as_uint(v.v[i]) & 0x7FFFFFFFu);
+                          }
+                        });
+        // own-block maximum goes through a second max slot before the
+        // barrier arrival so it is complete when the barrier opens
+        const uint32_t mow = warp_max_u32(mo);
+        if (lane_id() == 0) atomicMax(&ctl->maxslot[8], ((unsigned long long)s_seq << 32) | mow);
+        float xmax;
+        if (!warp_barrier_max(P, R, ctl, err, 0, m, xmax, 0)) return;
+        const float own = read_max_slot(ctl, 8);
+        if (nonfinite(xmax)) bad = 1;  // reference compress() rejects the whole local vector
+        q0 = q8_make(q8_scale(xmax));
+        vmax = fabsf(q8_decode(q8_encode(own, q0), q0.s));
+      }
       q = q8_make(q8_scale(vmax));
     }
     uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
@@ -301,7 +364,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
-                      store_pay<C>(dst, g0 - B.A, vlo, vhi, encode_v<C>(v, q, bad));
+                      store_pay<C>(dst, g0 - B.A, vlo, vhi, encode_v<C>(px(v), q, bad));
                     });
       warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
     }
@@ -311,6 +374,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   }
 
   // ---- reduce-scatter steps: fold block (r-s-1)%p, forward (or own it)
+  const bool own_via_inbox = slot_mode && C == kQuant8;  // owner re-quantises later, with the global scale
   for (int s = 0; s < p - 1; ++s) {
     const int b = (r - s - 1 + p) % p;
     const Blk B = get_blk(P, b);
@@ -326,7 +390,19 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       } else {
         for (int d = 1; d < p; ++d)
           store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
-        store_fv<E>(out, g0, lo, hi, decode_v<C>(pk, sc));
+        if (own_via_inbox)
+          store_pay<C>(slot_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+        else if (slot_mode)
+          store_pay<C>(R.slot, g0, vlo, vhi, pk);  // none/trunc16: C(D(wire)) == wire
+        else
+          store_fv<E>(out, g0, lo, hi, decode_v<C>(pk, sc));
+      }
+    };
+    auto publish_last = [&](uint32_t c, float sc) {
+      warp_publish_all(P, R, b, c, B.len, sc);
+      if (own_via_inbox && lane_id() == 0) {
+        if (c == 0) write_hdr(P, R.inbox, ag_slot(p, b), b, B.len, sc);
+        st_release_sys(flag_ptr(R.inbox, P.L, ag_slot(p, b), c), flag_word(sc));
       }
     };
 
@@ -340,10 +416,11 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         first = false;
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
-                        emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(v.x, decode_v<C>(v.in, sin)), q, bad), 0.f);
+                        emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
+                             0.f);
                       });
         if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
-        else warp_publish_all(P, R, b, c, B.len, 0.f);
+        else publish_last(c, 0.f);
       }
     } else {
       // pass A: fold into `out` (scratch for this block) and reduce the max
@@ -356,7 +433,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         first = false;
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
-                        const FV<E> acc = add_v(v.x, decode_v<C>(v.in, sin));
+                        const FV<E> acc = add_v(px(v.x), decode_v<C>(v.in, sin));
                         m = max(m, absmax_bits(acc));
                         store_fv<E>(out, g0, lo, hi, acc);
                       });
@@ -376,7 +453,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                         emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
                       });
         if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
-        else warp_publish_all(P, R, b, c, B.len, q.s);
+        else publish_last(c, q.s);
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
@@ -385,8 +462,36 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     stamp(P, wid, lr, 3 + 2 * s);
   }
 
-  // ---- allgather, receive side: decode every other owner's bytes
-  for (int k = 1; k < p; ++k) {
+  // ---- slot mode, quant8: the pipe re-compress (engine.py:407) needs the
+  // whole-vector scale of the summed vector. Every block's codes reach 127,
+  // so max|sum| = 127 * max_b s_b, known from the block scales in the
+  // allgather flag words: no pass over the sum, and the result equals the
+  // reference's compress(summed) scale exactly.
+  Q8 qs = q8_make(0.f);
+  if (own_via_inbox) {
+    float vmax = 0.f;
+    int ok = 1;
+    if (lane_id() == 0) {
+      for (int b = 0; b < p && ok; ++b) {
+        const Blk B = get_blk(P, b);
+        if (B.nch == 0) continue;
+        const uint64_t v = spin_flag(flag_ptr(R.inbox, P.L, ag_slot(p, b), 0), P, R, ctl, err, kPhAG,
+                                     (r - b + p) % p, b);
+        ok = v != 0;
+        vmax = fmaxf(vmax, __fmul_rn(127.f, __uint_as_float((uint32_t)v)));
+      }
+    }
+    __syncwarp();
+    if (!__shfl_sync(0xffffffffu, ok, 0)) return;
+    qs = q8_make(q8_scale(__shfl_sync(0xffffffffu, vmax, 0)));
+    if (wid == 0 && lane_id() == 0) *R.slot_scale = qs.s;
+  } else if (slot_mode && wid == 0 && lane_id() == 0) {
+    *R.slot_scale = 0.f;
+  }
+
+  // ---- allgather, receive side: every other owner's bytes (and, for the
+  // quant8 slot, the own block) -> out (decoded) or the compressed slot
+  for (int k = own_via_inbox ? 0 : 1; k < p; ++k) {
     const int b = (r + 1 + k) % p;  // own block is (r+1)%p
     const Blk B = get_blk(P, b);
     const int step = (r - b + p) % p;  // reference allgather step that delivers block b
@@ -401,8 +506,14 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
                       return load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
                     },
-                    [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const uint4& v) {
-                      store_fv<E>(out, g0, lo, hi, decode_v<C>(v, sin));
+                    [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const uint4& v) {
+                      if (!slot_mode) {
+                        store_fv<E>(out, g0, lo, hi, decode_v<C>(v, sin));
+                      } else if constexpr (C == kQuant8) {
+                        store_pay<C>(R.slot, g0, vlo, vhi, encode_v<C>(decode_v<C>(v, sin), qs, bad));
+                      } else {
+                        store_pay<C>(R.slot, g0, vlo, vhi, v);
+                      }
                     });
     }
   }

@@ -38,7 +38,9 @@ struct SlotHdr {               // written by the sender before each chunk flag
 
 struct RankCtx {
   const float* x;              // this rank's input vector (n)
-  float* out;                  // this rank's output vector (n)
+  float* out;                  // this rank's output vector (n); quant8 scratch in slot mode
+  uint8_t* slot;               // slot mode: C(sum) payload (n * width bytes), else null
+  float* slot_scale;           // slot mode: its whole-vector scale
   uint8_t* inbox;              // this rank's inbox (local HBM)
   uint8_t* peer[kMaxRanks];    // every rank's inbox as seen from this GPU
   int rank;
@@ -52,6 +54,7 @@ struct RingParams {
   uint32_t iteration;
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
   int p, codec, G;             // world size, codec tag, CTAs per rank (16 warp workers each)
+  int pre;                     // x is the raw gradient: apply the local D(C(.)) on load
   unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
 

@@ -110,12 +110,13 @@ class GpuEndpoint:
         _lib.call("gp_get_stats", self._comm, self.rank, ctypes.byref(s))
         return TrafficStats(int(s.messages), int(s.payload_bytes), int(s.frame_bytes))
 
-    def _launch(self, x: torch.Tensor, out: torch.Tensor, codec: int, iteration: int,
-                stream: torch.cuda.Stream) -> None:
+    def _launch(self, x: torch.Tensor, out: torch.Tensor | None, codec: int, iteration: int,
+                stream: torch.cuda.Stream, flags: int = 0, slot: torch.Tensor | None = None,
+                slot_scale: torch.Tensor | None = None) -> None:
         if self._poisoned:
             raise CollectiveError(f"endpoint {self.rank} is unusable after an earlier failure: {self._poisoned}")
-        _lib.call("gp_allreduce", self._comm, x.data_ptr(), out.data_ptr(), x.numel(), int(codec),
-                  int(iteration) & 0xFFFFFFFF, stream.cuda_stream)
+        _lib.call("gp_allreduce_ex", self._comm, x.data_ptr(), _ptr(out), _ptr(slot), _ptr(slot_scale),
+                  x.numel(), int(codec), int(flags), int(iteration) & 0xFFFFFFFF, stream.cuda_stream)
 
     def _check_errors(self, n: int) -> None:
         """After the launching stream completed: raise what the device latched."""
@@ -128,6 +129,10 @@ class GpuEndpoint:
         if isinstance(err, CollectiveError):
             self._poisoned = str(err)
         return err
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
 
 
 def raise_for(e, p: int, n: int, timeout_s: float) -> Exception:
@@ -204,8 +209,8 @@ class EmulatedEndpoint(GpuEndpoint):
     """Endpoint of an EmulatedTransport: its calls rendezvous with the other
     virtual ranks; the last arrival launches the ring for everyone."""
 
-    def _launch(self, x, out, codec, iteration, stream):
-        self._gen = self._transport._arrive(self.rank, x, out, codec, iteration, stream)
+    def _launch(self, x, out, codec, iteration, stream, flags=0, slot=None, slot_scale=None):
+        self._gen = self._transport._arrive(self.rank, x, out, codec, iteration, stream, flags, slot, slot_scale)
 
     def _check_errors(self, n: int) -> None:
         self._transport._finish(getattr(self, "_gen", None))
@@ -242,14 +247,14 @@ class EmulatedTransport:
     def endpoint(self, rank: int) -> EmulatedEndpoint:
         return self._eps[rank]
 
-    def _arrive(self, rank, x, out, codec, iteration, stream) -> _Generation:
+    def _arrive(self, rank, x, out, codec, iteration, stream, flags=0, slot=None, slot_scale=None) -> _Generation:
         ev = torch.cuda.Event()
         ev.record(stream)
         with self._cv:
             gen = self._cur
             if rank in gen.slots:
                 raise CollectiveError(f"rank {rank} entered the same allreduce twice")
-            gen.slots[rank] = (x, out, int(codec), int(iteration), x.numel(), ev)
+            gen.slots[rank] = (x, out, int(codec), int(iteration), x.numel(), ev, int(flags), slot, slot_scale)
             if len(gen.slots) == self.world_size:
                 self._launch_all(gen)
                 self._cur = _Generation()
@@ -268,19 +273,23 @@ class EmulatedTransport:
         p = self.world_size
         args = [gen.slots[r] for r in range(p)]
         gen.launched = True
-        if len({a[4] for a in args}) != 1 or len({a[2] for a in args}) != 1 or len({a[3] for a in args}) != 1:
+        if len({a[4] for a in args}) != 1 or len({a[2] for a in args}) != 1 or len({a[3] for a in args}) != 1 \
+                or len({a[6] for a in args}) != 1:
             gen.error = CollectiveError("reduce-scatter step 0: ranks disagree on vector length, codec or "
                                         "iteration (unequal vector lengths across ranks?)")
             return
         gen.n = args[0][4]
         ins = (ctypes.c_void_p * p)(*[a[0].data_ptr() for a in args])
-        outs = (ctypes.c_void_p * p)(*[a[1].data_ptr() for a in args])
+        outs = (ctypes.c_void_p * p)(*[_ptr(a[1]) for a in args])
+        slots = (ctypes.c_void_p * p)(*[_ptr(a[7]) for a in args])
+        scales = (ctypes.c_void_p * p)(*[_ptr(a[8]) for a in args])
         for a in args:
             self._stream.wait_event(a[5])
-            a[0].record_stream(self._stream)
-            a[1].record_stream(self._stream)
-        _lib.call("gp_allreduce_emulated", self._comm, ins, outs, gen.n, args[0][2], args[0][3] & 0xFFFFFFFF,
-                  self._stream.cuda_stream)
+            for t in (a[0], a[1], a[7], a[8]):
+                if t is not None:
+                    t.record_stream(self._stream)
+        _lib.call("gp_allreduce_emulated_ex", self._comm, ins, outs, slots, scales, gen.n, args[0][2], args[0][6],
+                  args[0][3] & 0xFFFFFFFF, self._stream.cuda_stream)
         gen.done = torch.cuda.Event()
         gen.done.record(self._stream)
         gen.slots = {}
