@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--ctas", type=int, default=32,
                     help="CTAs the ring kernel may occupy per GPU (the rest keep computing)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--fused", type=int, default=1,
+                    help="one comm kernel per step (pre-compress + ring + re-compress fused)")
     ap.add_argument("--channels-last", type=int, default=1,
                     help="feed NHWC activations to cuDNN (no NCHW<->NHWC transposes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -275,7 +277,7 @@ def our_arm(args, ws, rank, local):
             return x_buf, y_buf
         return x_dev, y_dev
 
-    eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True)
+    eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True, fused=bool(args.fused))
     loss_host = torch.zeros(total_steps + 2, dtype=torch.float32).pin_memory()
 
     def barrier():
@@ -378,7 +380,8 @@ def our_arm(args, ws, rank, local):
                 "algorithmic_bytes_per_launch": wire}
     else:
         copy_gbs = 8 * n / (iso["copy_4n"] * 1e-3) / 1e9
-        dom = max(("update", "compress", "recompress"), key=lambda k: avg.get(k, 0.0))
+        dom = max([k for k in ("update", "compress", "recompress") if k in kernels],
+                  key=lambda k: avg.get(k, 0.0))
         name = {"update": "consume_update_kernel", "compress": "roundtrip_kernel",
                 "recompress": "encode_kernel"}[dom]
         kd = kernels[dom]
@@ -393,7 +396,12 @@ def our_arm(args, ws, rank, local):
                 "note": "at this vector size (%d fp32) launch/ramp latency bounds every kernel: torch's own "
                         "copy of 8n bytes reaches %.0f GB/s by the same method" % (n, copy_gbs),
                 "algorithmic_bytes_per_launch": algo[dom]}
-    per_iter_launches = 1 + (2 if q8 else 1) + (1 if N > 1 else 0) + (2 if q8 else 1)
+    # our kernels per step: consume_update + (fused) one ring kernel, or at p=1
+    # the encode (absmax+encode for quant8); unfused adds pre-compress/re-compress
+    if eng.fused:
+        per_iter_launches = 1 + (1 if N > 1 else (2 if q8 else 1))
+    else:
+        per_iter_launches = 1 + (2 if q8 else 1) + (1 if N > 1 else 0) + (2 if q8 else 1)
 
     allreduce = None
     if N > 1 and not args.no_allreduce_sweep:
@@ -485,16 +493,24 @@ def isolated_kernels(eng, codec, N, dev, reps=20):
     torch.cuda.synchronize(dev)
     cp_src = torch.empty(n, dtype=torch.float32, device=dev)
     cp_dst = torch.empty_like(cp_src)
+    g = eng.fm.grads
     out = {
         "copy_4n": timeit(lambda: cp_dst.copy_(cp_src)),  # torch copy: 4n read + 4n write, same method
         "update": timeit(lambda: _lib.call("gp_consume_update", w_scratch.data_ptr(), int(slot.codec),
                                            slot.payload.data_ptr(), slot.status.scale_view.data_ptr(), n, lr,
                                            N, s.cuda_stream)),
-        "compress": timeit(lambda: roundtrip_async(eng.fm.grads, codec, loc, st, s.cuda_stream)),
-        "recompress": timeit(lambda: encode_async(loc, codec, slot.payload, st, s.cuda_stream)),
     }
+    if not eng.fused:
+        out["compress"] = timeit(lambda: roundtrip_async(g, codec, loc, st, s.cuda_stream))
+    if N == 1 or not eng.fused:
+        out["recompress"] = timeit(lambda: encode_async(g, codec, slot.payload, st, s.cuda_stream))
     if N > 1:
-        out["ring"] = timeit(lambda: allreduce_into(loc, eng.summed, eng.ep, codec, 0, s), sync_ranks=True)
+        if eng.fused:  # the comm stream's single kernel: D(C(g)) -> ring -> C(sum) into the slot
+            out["ring"] = timeit(lambda: allreduce_into(g, eng.summed, eng.ep, codec, 0, s, precompress=True,
+                                                        slot=slot.payload, slot_scale=slot.status.scale_view),
+                                 sync_ranks=True)
+        else:
+            out["ring"] = timeit(lambda: allreduce_into(loc, eng.summed, eng.ep, codec, 0, s), sync_ranks=True)
         endpoint_wait(eng.ep, n, s)
     return out
 

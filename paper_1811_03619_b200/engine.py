@@ -181,8 +181,14 @@ class RankEngine:
     """One rank's Pipe-SGD loop on one GPU (enqueue-only host thread)."""
 
     def __init__(self, rank: int, world: int, endpoint: GpuEndpoint, fm: FlatModel, config: RunConfig,
-                 batch_fn: BatchFn, trace: bool = True, grad_fn=None):
+                 batch_fn: BatchFn, trace: bool = True, grad_fn=None, fused: bool = True):
+        """fused=True (default): the comm stream runs ONE kernel per iteration —
+        the ring with the local pre-compress applied on load and the pipe
+        re-compress written as the slot by its allgather (gp_allreduce_ex);
+        the raw gradient sits in K alternating buffers. fused=False keeps the
+        separate pre-compress / ring / re-compress kernels (reference order)."""
         self.rank, self.world, self.ep, self.fm, self.cfg = rank, world, endpoint, fm, config
+        self.fused = fused
         self.batch_fn = batch_fn
         self.grad_fn = grad_fn
         self.dev = fm.params.device
@@ -193,6 +199,8 @@ class RankEngine:
         self.events: list = []  # (iteration, stage, ev0, ev1, consumed)
         K = max(config.depth, 1)
         self.K = K
+        if fused:
+            fm.ensure_grad_buffers(K)
         w = config.codec.bytes_per_elem
         with torch.cuda.device(self.dev):
             self.local = [torch.empty(self.n, dtype=torch.float32, device=self.dev) for _ in range(K)]
@@ -246,8 +254,10 @@ class RankEngine:
             self.early_params.append((t, self.fm.params.clone()))
 
     def _compute_local(self, t: int) -> None:
-        """fwd + bwd + whole-vector D(C(grad)) into local[t % K] (engine.py:323-336)."""
+        """fwd + bwd (+ whole-vector D(C(grad)) when not fused) (engine.py:323-336)."""
         i = t % self.K
+        if self.fused:
+            self.fm.use_grad_buffer(i)
         e0 = self._ev(self.cs) if self.tracing else None
         if self.grad_fn is not None:
             self.cs.synchronize()
@@ -259,16 +269,20 @@ class RankEngine:
             loss = self.fm.loss_and_grad(x, y)
             self.losses[t].copy_(loss)
         e1 = self._ev(self.cs) if self.tracing else None
-        roundtrip_async(self.fm.grads, self.cfg.codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+        if not self.fused:
+            roundtrip_async(self.fm.grads, self.cfg.codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
         self.ev_local[i].record(self.cs)
         if self.tracing:
             self._rec(t, STAGE_BACKWARD, e0, e1)
-            self._rec(t, STAGE_COMPRESS, e1, self._ev(self.cs))
+            if not self.fused:
+                self._rec(t, STAGE_COMPRESS, e1, self._ev(self.cs))
         if self.cfg.eval_interval and self.rank == 0 and t % self.cfg.eval_interval == 0:
             self.eval_points.append((t, self.fm.params.clone()))
 
     def _communicate(self, t: int, requant: bool) -> _Slot:
         """Comm stream: ring(local[t]) -> (pipe) C(sum) into slot t."""
+        if self.fused:
+            return self._communicate_fused(t, requant)
         i = t % self.K
         self.ms.wait_event(self.ev_local[i])
         e0 = self._ev(self.ms) if self.tracing else None
@@ -291,6 +305,35 @@ class RankEngine:
                 self._rec(t, "ring", e0, e1)
             if requant:
                 self._rec(t, "recompress", e1, ready)
+        self.buffer.put(t, slot, ready)
+        return slot
+
+    def _communicate_fused(self, t: int, requant: bool) -> _Slot:
+        """Comm stream, one kernel: raw grad -> D(C(.)) -> ring -> (pipe) C(sum)
+        written straight into slot t (p == 1: C(D(C(g))) == C(g), one encode)."""
+        i = t % self.K
+        g = self.fm.grad_bufs[i]
+        self.ms.wait_event(self.ev_local[i])
+        e0 = self._ev(self.ms) if self.tracing else None
+        codec = self.cfg.codec
+        if requant:
+            slot = self.slots[i]
+            if self.world > 1:
+                allreduce_into(g, self.summed, self.ep, codec, t, self.ms, precompress=True,
+                               slot=slot.payload, slot_scale=slot.status.scale_view)
+            else:
+                encode_async(g, codec, slot.payload, slot.status, self.ms.cuda_stream)
+        else:
+            slot = self.sync_slots[i]
+            if self.world > 1:
+                allreduce_into(g, self.summed, self.ep, codec, t, self.ms, precompress=True)
+            else:
+                roundtrip_async(g, codec, self.local[i], self.local_status[i], self.ms.cuda_stream)
+        ready = torch.cuda.Event(enable_timing=self.tracing)
+        ready.record(self.ms)
+        if self.tracing:
+            self._rec(t, STAGE_ALLREDUCE, e0, ready)
+            self._rec(t, "ring" if self.world > 1 else "recompress", e0, ready)
         self.buffer.put(t, slot, ready)
         return slot
 
@@ -372,7 +415,8 @@ class RankEngine:
         self.cs.synchronize()
         self.ms.synchronize()
         self.ep._check_errors(self.n)
-        if any(int(s.t[1].item()) for s in self.local_status):
+        if any(int(s.t[1].item()) for s in self.local_status) or \
+                any(int(s.status.t[1].item()) for s in self.slots):
             raise CodecError("refusing to compress non-finite values")
         losses = self.losses.cpu().numpy()
         metrics = [(t, start_ev.elapsed_time(e), float(losses[t])) for t, e in sorted(self.iter_done.items())]
@@ -391,9 +435,16 @@ class RankEngine:
 
 # ----------------------------------------------------------------- clusters
 
-def _make_transport(workers: int, timeout_s: float, max_elems: int):
+# SMs the ring kernel may occupy while the compute stream runs the next
+# iteration (the rest of the 148 stay free for forward/backward); the ring
+# reaches ~300-500 GB/s at 32 CTAs on 2xB200 (profiles/), far above what a
+# pipelined step needs to stay compute-bound.
+COMM_CTAS = 32
+
+
+def _make_transport(workers: int, timeout_s: float, max_elems: int, ctas: int = COMM_CTAS):
     if torch.cuda.device_count() >= workers:
-        return GpuTransport(workers, timeout_s=timeout_s, max_elems=max_elems)
+        return GpuTransport(workers, timeout_s=timeout_s, max_elems=max_elems, ctas=ctas)
     return EmulatedTransport(workers, timeout_s=timeout_s, max_elems=max_elems)
 
 
@@ -414,7 +465,8 @@ class DeviceDataset:
 
 def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_s: float = 0.0,
                        byte_time_s: float = 0.0, batch_provider=None, timeout_s: float = 30.0,
-                       transport=None, grad_fn=None, trace: bool = True) -> list[WorkerResult]:
+                       transport=None, grad_fn=None, trace: bool = True, fused: bool = True,
+                       comm_ctas: int = COMM_CTAS) -> list[WorkerResult]:
     """Run a full training job with all ranks as threads of this process
     (engine.py:563-618), one GPU per rank (GpuTransport) or all ranks on one
     GPU (EmulatedTransport) when there are fewer GPUs than workers.
@@ -430,7 +482,7 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
         model = ModelSpec(model.kind, tuple(model.layer_dims))
     n = model.num_params
     own_transport = transport is None
-    tr = transport or _make_transport(workers, timeout_s, max(n, 1))
+    tr = transport or _make_transport(workers, timeout_s, max(n, 1), comm_ctas)
     shards = [np.arange(r % workers, dataset.features.shape[0], workers) for r in range(workers)]
     if batch_provider is None and grad_fn is None:
         for r in range(workers):
@@ -455,7 +507,7 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
                         shards[rank][rng.choice(len(shards[rank]), size=config.batch_size, replace=False)]
                     return data.gather(idx)
 
-                eng = RankEngine(r, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn)
+                eng = RankEngine(r, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn, fused=fused)
                 ipe = max(1, len(shards[r]) // config.batch_size)
                 torch.cuda.synchronize(dev)
                 barrier.wait()

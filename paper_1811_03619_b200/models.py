@@ -154,26 +154,52 @@ class FlatModel:
     aligned; parameter order is module.parameters() order (for SpecNet that
     is exactly the reference's flat layout)."""
 
-    def __init__(self, module: nn.Module, device, init_flat: np.ndarray | None = None):
+    def __init__(self, module: nn.Module, device, init_flat: np.ndarray | None = None, grad_buffers: int = 1):
         self.module = module.to(device)
-        plist = [p for p in self.module.parameters() if p.requires_grad]
-        self.num_params = sum(p.numel() for p in plist)
+        self.plist = [p for p in self.module.parameters() if p.requires_grad]
+        self.num_params = sum(p.numel() for p in self.plist)
         self.params = torch.empty(self.num_params, dtype=torch.float32, device=device)
-        self.grads = torch.zeros(self.num_params, dtype=torch.float32, device=device)
+        # K flat gradient buffers: the fused ring reads buffer t % K while the
+        # next backward writes another one
+        self.grad_bufs = [torch.zeros(self.num_params, dtype=torch.float32, device=device)
+                          for _ in range(max(1, grad_buffers))]
+        self._grad_views = [[] for _ in self.grad_bufs]
         off = 0
-        for p in plist:
+        for p in self.plist:
             k = p.numel()
             view = self.params[off:off + k].view_as(p)
             view.copy_(p.data)
             p.data = view
-            # autograd accumulates in place into an existing .grad, so the
-            # backward pass writes straight into the flat gradient buffer
-            p.grad = self.grads[off:off + k].view_as(p)
+            for i, g in enumerate(self.grad_bufs):
+                self._grad_views[i].append(g[off:off + k].view_as(p))
             off += k
+        self.use_grad_buffer(0)
         if init_flat is not None:
             if init_flat.size != self.num_params:
                 raise ConfigError(f"init vector has {init_flat.size} values, model has {self.num_params}")
             self.params.copy_(torch.from_numpy(np.ascontiguousarray(init_flat, np.float32)))
+
+    def ensure_grad_buffers(self, k: int) -> None:
+        while len(self.grad_bufs) < k:
+            g = torch.zeros(self.num_params, dtype=torch.float32, device=self.params.device)
+            views, off = [], 0
+            for p in self.plist:
+                views.append(g[off:off + p.numel()].view_as(p))
+                off += p.numel()
+            self.grad_bufs.append(g)
+            self._grad_views.append(views)
+
+    def use_grad_buffer(self, i: int) -> torch.Tensor:
+        """Point every parameter's .grad at flat buffer i (autograd accumulates
+        in place into an existing .grad, so backward writes straight into it)."""
+        self._cur = i
+        for p, v in zip(self.plist, self._grad_views[i]):
+            p.grad = v
+        return self.grad_bufs[i]
+
+    @property
+    def grads(self) -> torch.Tensor:
+        return self.grad_bufs[self._cur]
 
     def zero_grad(self):
         self.grads.zero_()

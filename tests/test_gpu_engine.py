@@ -57,8 +57,9 @@ def oracle_grad_fn(data, net, p, seed, batch_size):
     return fn
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "unfused"])
 @pytest.mark.parametrize("case", ENGINE_CASES, ids=lambda c: c[0])
-def test_engine_bit_exact_with_oracle_gradients(P, gold, blobs, case):
+def test_engine_bit_exact_with_oracle_gradients(P, gold, blobs, case, fused):
     from paper_1811_03619_b200.engine import RunConfig, run_inproc_cluster
     from paper_1811_03619_b200.models import ModelSpec
     name, m, mode, codec, p, T, K, warm, lr, bs, dec = case
@@ -67,7 +68,7 @@ def test_engine_bit_exact_with_oracle_gradients(P, gold, blobs, case):
     net = OE.Net(kind, dims)
     cfg = RunConfig(mode=mode, iterations=T, learning_rate=lr, codec=codec, depth=K, batch_size=bs,
                     warmup_epochs=warm, seed=7, lr_decay_every=dec, lr_decay_factor=0.5)
-    res = run_inproc_cluster(p, cfg, blobs, spec, grad_fn=oracle_grad_fn(blobs, net, p, 7, bs))
+    res = run_inproc_cluster(p, cfg, blobs, spec, grad_fn=oracle_grad_fn(blobs, net, p, 7, bs), fused=fused)
     for r in res:
         assert_bits_equal(r.params, gold[name], f"{name} rank {r.rank}")
     losses = [x[2] for x in res[0].metrics]
