@@ -223,13 +223,21 @@ def reference_arm(args, ws, rank):
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+MODEL_NAMES = {"c1": ("C1 (configs[0]): MNIST-shaped MLP 784-500-500-10", "MLP 784-500-500-10"),
+               "c2": ("C2 (BASELINE.json configs[1]): CIFAR-10-shaped small CNN", "SmallCNN 3conv+2fc"),
+               "c3": ("C3 (configs[2]): AlexNet ImageNet-shaped", "torchvision AlexNet"),
+               "c4": ("C4 (configs[3]): ResNet-50 ImageNet-shaped", "torchvision ResNet-50")}
+
+
 def workload_config(args, n, N):
-    return {"workload": f"C2 (BASELINE.json configs[1]): CIFAR-10-shaped small CNN, Pipe-SGD width {args.depth}, "
+    title, model = MODEL_NAMES.get(args.model, (args.model, args.model))
+    width = args.depth if args.mode == "pipe_sgd" else 1
+    return {"workload": f"{title}, {'Pipe-SGD' if args.mode == 'pipe_sgd' else 'D-Sync'} width {width}, "
                         f"{args.codec} ring compression",
-            "model": "SmallCNN 3conv+2fc", "params": n, "global_batch": args.global_batch,
-            "per_gpu_batch": args.global_batch // max(N, 1), "image": [3, 32, 32], "codec": args.codec,
-            "mode": args.mode, "depth": args.depth, "parallelism": f"dp{N}",
-            "l2": "not flushed: each step streams the CNN activations of the per-GPU batch plus the 18.8 MB "
+            "model": model, "params": n, "global_batch": args.global_batch,
+            "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
+            "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
+            "l2": "not flushed: each step streams the model's activations for the per-GPU batch plus the "
                   "gradient, weights and slots through HBM"}
 
 
@@ -293,7 +301,7 @@ def our_arm(args, ws, rank, local):
         start.record(eng.cs)
         eng.ms.wait_stream(eng.cs)
         for t in range(t0, t0 + steps):
-            eng.step(t)
+            step(t)
             if e2e:  # device->host read of the step's loss (async into pinned memory)
                 with torch.cuda.stream(eng.cs):
                     loss_host[t:t + 1].copy_(eng.losses[t:t + 1], non_blocking=True)
@@ -306,21 +314,27 @@ def our_arm(args, ws, rank, local):
         ms = max(start.elapsed_time(end_c), start.elapsed_time(end_m))
         return max_over_ranks(ms, dev), list(eng.events)
 
+    pipe = args.mode == "pipe_sgd"
+    step = eng.step if pipe else eng.step_sync
     with torch.cuda.device(dev), torch.cuda.stream(eng.cs):
-        eng.prime(1)
+        if pipe:
+            eng.prime(1)
         t = 1
         for _ in range(args.warmup):
-            eng.step(t)
+            step(t)
             t += 1
         with ClockSampler(local) as clk:
             ms_total, events = timed_region(t, args.steps, e2e=False)
         t += args.steps
         for _ in range(2):
-            eng.step(t)
+            step(t)
             t += 1
         e2e_ms, _ = timed_region(t, args.steps, e2e=True)
         t += args.steps
-        eng.drain(t - 1)
+        if pipe:
+            eng.drain(t - 1)
+        else:
+            eng.drain_sync()
         torch.cuda.synchronize(dev)
     ep._check_errors(n)
     if any(int(s.t[1].item()) for s in eng.local_status):
@@ -405,7 +419,7 @@ def our_arm(args, ws, rank, local):
 
     allreduce = None
     if N > 1 and not args.no_allreduce_sweep:
-        allreduce = ring_vs_nccl(ep, args.codec, N, dev, [n, 1 << 26])
+        allreduce = ring_vs_nccl(ep, args.codec, N, dev, [1024, n, 1 << 26], ctas_list=(0, 148))
 
     line = None
     if rank == 0:
@@ -424,7 +438,16 @@ def our_arm(args, ws, rank, local):
                 "samples_per_s": value * args.global_batch}
         if allreduce:
             line["allreduce"] = allreduce
-        line["timing_model"] = timing_model(avg, n, N, w)
+            big = allreduce[-1]
+            wire_big = 2 * (N - 1) / N * big["n"] * w
+            key = f"{args.codec}@148ctas"
+            ach = wire_big / (big[key]["ms"] * 1e-3) / 1e9
+            line["roofline_large_bucket"] = {
+                "kernel": roof["kernel"], "n": big["n"], "bound": "nvlink", "achieved": ach,
+                "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "ctas": 148,
+                "note": "the same ring kernel alone on a 256 MiB fp32 bucket with every SM (standalone "
+                        "allreduce configuration); the engine runs it on 32 CTAs beside the CNN"}
+        line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms)
     return line
 
 
@@ -515,20 +538,27 @@ def isolated_kernels(eng, codec, N, dev, reps=20):
     return out
 
 
-def ring_vs_nccl(ep, codec, N, dev, sizes):
+def ring_vs_nccl(ep, codec, N, dev, sizes, ctas_list=(0,)):
+    """Back-to-back allreduce of each size (device time, max over ranks):
+    our ring with `codec` and with none at each CTA budget (0 = the
+    engine's), and NCCL all_reduce on the same buffer."""
     import torch
     import torch.distributed as dist
+    from paper_1811_03619_b200 import _lib
     from paper_1811_03619_b200.collective import allreduce_into, endpoint_wait
     out = []
     s = torch.cuda.Stream(dev)
+    base = ep.info()["ctas"]
     for n in sizes:
         x = torch.randn(n, device=dev)
         y = torch.empty_like(x)
         res = {"n": n, "bytes_fp32": 4 * n}
-        for name in (codec, "none", "nccl"):
-            if name in res:
-                continue
+        runs = [(c, g) for g in ctas_list for c in dict.fromkeys((codec, "none"))] + [("nccl", 0)]
+        for name, g in runs:
             it = 20 if n < (1 << 24) else 8
+            key = name if (g == 0 or name == "nccl") else f"{name}@{g}ctas"
+            if name != "nccl":
+                _lib.call("gp_comm_set_tuning", ep._comm, int(g or base), 0.0)
 
             def run():
                 if name == "nccl":
@@ -547,25 +577,50 @@ def ring_vs_nccl(ep, codec, N, dev, sizes):
                 run()
             b.record(s)
             b.synchronize()
-            t = torch.tensor([a.elapsed_time(b) / it], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = max_over_ranks(a.elapsed_time(b) / it, dev)
             if name != "nccl":
                 endpoint_wait(ep, n, s)
-            res[name] = {"ms": ms, "busbw_gbs": 2 * (N - 1) / N * 4 * n / (ms * 1e-3) / 1e9}
+            res[key] = {"ms": ms, "busbw_gbs": 2 * (N - 1) / N * 4 * n / (ms * 1e-3) / 1e9}
+        _lib.call("gp_comm_set_tuning", ep._comm, int(base), 0.0)
         out.append(res)
     return out
 
 
-def timing_model(avg, n, N, w):
-    """Paper Eq. (4)/(5) (timing.py:109-132) with GPU-measured stage times:
-    pipe iteration = max(update + compute, comm)."""
+def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms):
+    """The paper's timing model (timing.py:97-132, harness.py:667-720) with
+    GPU-measured symbols. Ring: Eq. 5 T = 2(p-1)a + 2(p-1)/p n b (+ n g + S
+    folded into a: the fused kernel overlaps its reduction with the transfer),
+    with a and b fitted like the reference's calibrate() (ping + flood) from
+    the ring itself at a 4 KiB and a 256 MiB bucket; prediction for the step's
+    gradient vs the measured isolated ring. Iteration: Eq. 4 (pipe) / Eq. 2
+    (sync) from the measured stage times vs the measured step."""
+    from paper_1811_03619_b200 import timing as T
     upd = avg.get("update", 0.0) + avg.get("compress", 0.0)
     comp = avg.get("backward", 0.0)
     comm = avg.get("allreduce", 0.0)
-    return {"update_ms": upd, "compute_ms": comp, "comm_ms": comm,
-            "predicted_pipe_ms": max(upd + comp, comm), "predicted_sync_ms": upd + comp + comm,
-            "bound": "compute" if upd + comp >= comm else "communication"}
+    out = {"update_ms": upd, "compute_ms": comp, "comm_ms_in_pipeline": comm}
+    stages = T.StageTimes(update=upd / 1e3, forward=0.0, backward=comp / 1e3, comm=comm / 1e3)
+    out["eq4_pipe_ms"] = T.t_pipe_limited(1, stages) * 1e3
+    out["eq2_sync_ms"] = T.t_sync_total(1, stages) * 1e3
+    out["measured_step_ms"] = step_ms
+    out["eq4_over_measured"] = out["eq4_pipe_ms"] / step_ms
+    out["bound"] = "compute" if upd + comp >= comm else "communication"
+    if allreduce and N > 1:
+        small, big = allreduce[0], allreduce[-1]
+        wb = lambda m: 2 * (N - 1) / N * m * w  # wire bytes per rank
+        t_small, t_big = small[codec]["ms"] * 1e-3, big[codec]["ms"] * 1e-3
+        beta = (t_big - t_small) / (wb(big["n"]) - wb(small["n"]))
+        alpha = max(0.0, (t_small - wb(small["n"]) * beta) / (2 * (N - 1)))
+        params = T.ClusterParams(workers=N, latency_s=alpha, byte_time_s=beta / 2, model_bytes=n * w)
+        pred = T.ring_comm_time(params)  # 2(p-1)/p * n * (beta/2) * 2 == wire bytes * beta
+        mid = allreduce[1]
+        meas = mid[codec]["ms"] * 1e-3  # same back-to-back method as the calibration points
+        out.update({"alpha_us": alpha * 1e6, "beta_gbs": 1 / beta / 1e9 if beta > 0 else None,
+                    "eq5_ring_pred_ms": pred * 1e3, "ring_measured_ms": meas * 1e3,
+                    "ring_isolated_barrier_aligned_ms": iso.get("ring"),
+                    "eq5_over_measured": pred / meas if meas else None,
+                    "within_25pct": bool(meas and abs(pred / meas - 1) <= 0.25)})
+    return out
 
 
 def main():

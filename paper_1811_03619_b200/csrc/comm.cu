@@ -135,6 +135,8 @@ uint32_t pick_chunk(uint64_t n, int p, int G, int codec) {
   const uint64_t lo = std::max<uint64_t>(kMinChunk, round_up(min_bytes / w, kMinChunk));
   const uint64_t hi = std::max<uint64_t>(lo, round_up(max_bytes / w, kMinChunk));
   const uint64_t maxblk = (n + p - 1) / p + 16;
+  // chunk indexing depends on G, so G is a communicator-wide setting (the
+  // transports pass the same CTA budget on every rank and check it)
   const uint64_t workers = (uint64_t)G * kRingWarps * per_warp;
   const uint64_t ch = round_up((maxblk + workers - 1) / workers, kMinChunk);
   return (uint32_t)std::max(lo, std::min(hi, ch));

@@ -316,7 +316,7 @@ class EmulatedTransport:
             self._comm = None
 
 
-def exchange_handles(handle: bytes, max_elems: int, device: int, group=None) -> bytes:
+def exchange_handles(handle: bytes, max_elems: int, device: int, group=None, ctas: int = 0) -> bytes:
     """All-gather every rank's 64-byte inbox IPC handle over the process
     group (any backend) and validate that the communicator geometry agrees;
     returns the rank-ordered handle blob gp_comm_connect_ipc expects."""
@@ -324,9 +324,12 @@ def exchange_handles(handle: bytes, max_elems: int, device: int, group=None) -> 
 
     world = dist.get_world_size(group)
     gathered = [None] * world
-    dist.all_gather_object(gathered, (bytes(handle), int(max_elems), int(device), _host_id()), group=group)
+    dist.all_gather_object(gathered, (bytes(handle), int(max_elems), int(device), _host_id(), int(ctas)),
+                           group=group)
     if len({g[1] for g in gathered}) != 1:
         raise ConfigError("all ranks must create the transport with the same max_elems")
+    if len({g[4] for g in gathered}) != 1:
+        raise ConfigError("all ranks must give the ring the same CTA budget (chunking depends on it)")
     if len({g[3] for g in gathered}) != 1:
         raise ConfigError("ProcessGroupTransport spans one node only (NVLink peer memory)")
     if len({g[2] for g in gathered}) != world:
@@ -334,6 +337,12 @@ def exchange_handles(handle: bytes, max_elems: int, device: int, group=None) -> 
     if any(len(g[0]) != 64 for g in gathered):
         raise ConfigError("malformed IPC handle")
     return b"".join(g[0] for g in gathered)
+
+
+def ep_ctas(comm) -> int:
+    o = (ctypes.c_int64 * 8)()
+    _lib.call("gp_comm_info", comm, o)
+    return int(o[4])
 
 
 def _host_id() -> str:
@@ -362,7 +371,7 @@ class ProcessGroupTransport:
         if world > 1:
             h = ctypes.create_string_buffer(64)
             _lib.call("gp_comm_ipc_handle", comm, h)
-            blob = exchange_handles(h.raw, int(max_elems), int(device), group)
+            blob = exchange_handles(h.raw, int(max_elems), int(device), group, ctas=ep_ctas(comm))
             _lib.call("gp_comm_connect_ipc", comm, blob)
             dist.barrier(group)
         return GpuEndpoint(rank, world, torch.device("cuda", device), comm, timeout_s)

@@ -75,6 +75,15 @@ def _exchange_same_device(rank, world):
     return "no error"
 
 
+def _exchange_bad_ctas(rank, world):
+    from paper_1811_03619_b200.transport import exchange_handles
+    try:
+        exchange_handles(bytes(64), 10, device=rank, ctas=16 + rank)
+    except Exception as e:  # noqa: BLE001
+        return type(e).__name__
+    return "no error"
+
+
 def _max_over_ranks(rank, world):
     import bench
     return bench.max_over_ranks(1.5 + rank)
@@ -87,6 +96,7 @@ def test_ipc_handle_exchange_gloo():
 def test_ipc_handle_exchange_rejects_mismatched_geometry():
     assert _run("_exchange_bad_capacity") == {0: "ConfigError", 1: "ConfigError"}
     assert _run("_exchange_same_device") == {0: "ConfigError", 1: "ConfigError"}
+    assert _run("_exchange_bad_ctas") == {0: "ConfigError", 1: "ConfigError"}
 
 
 def test_bench_max_over_ranks_gloo():
