@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "Pipe-SGD iters/sec & compressed ring-allreduce bus GB/s at 1/2/4/8 B200"
 NVLINK_PEAK_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction (MEASURED_PEAKS has no NVLink)
 L2_BYTES = 126.5 * 2**20
+FULL_CTAS = 592  # 128-thread ring CTAs filling every SM (16 warps per SM)
 
 
 def parse():
@@ -47,8 +48,8 @@ def parse():
     ap.add_argument("--mode", default="pipe_sgd")
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--global-batch", type=int, default=512)
-    ap.add_argument("--ctas", type=int, default=32,
-                    help="CTAs the ring kernel may occupy per GPU (the rest keep computing)")
+    ap.add_argument("--ctas", type=int, default=128,
+                    help="128-thread CTAs the ring kernel may occupy per GPU beside the compute stream")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--fused", type=int, default=1,
                     help="one comm kernel per step (pre-compress + ring + re-compress fused)")
@@ -419,7 +420,7 @@ def our_arm(args, ws, rank, local):
 
     allreduce = None
     if N > 1 and not args.no_allreduce_sweep:
-        allreduce = ring_vs_nccl(ep, args.codec, N, dev, [1024, n, 1 << 26], ctas_list=(0, 148))
+        allreduce = ring_vs_nccl(ep, args.codec, N, dev, [1024, n, 1 << 26], ctas_list=(0, FULL_CTAS))
 
     line = None
     if rank == 0:
@@ -440,13 +441,13 @@ def our_arm(args, ws, rank, local):
             line["allreduce"] = allreduce
             big = allreduce[-1]
             wire_big = 2 * (N - 1) / N * big["n"] * w
-            key = f"{args.codec}@148ctas"
+            key = f"{args.codec}@{FULL_CTAS}ctas"
             ach = wire_big / (big[key]["ms"] * 1e-3) / 1e9
             line["roofline_large_bucket"] = {
                 "kernel": roof["kernel"], "n": big["n"], "bound": "nvlink", "achieved": ach,
-                "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "ctas": 148,
+                "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "ctas": FULL_CTAS,
                 "note": "the same ring kernel alone on a 256 MiB fp32 bucket with every SM (standalone "
-                        "allreduce configuration); the engine runs it on 32 CTAs beside the CNN"}
+                        "allreduce configuration); the engine runs it on 128 CTAs beside the CNN"}
         line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms)
     return line
 

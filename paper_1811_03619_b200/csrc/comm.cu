@@ -89,11 +89,15 @@ int alloc_inbox(gp_comm* c, int i) {
   return GP_OK;
 }
 
-int default_ctas(int device) {
+int sm_count(int device) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  return std::max(1, sms);
+  return sms;
 }
+
+// Default CTA budget: 16 warps per SM on every SM (one 512-thread CTA, or
+// four 128-thread CTAs, per SM).
+int default_ctas(int device) { return std::max(1, sm_count(device) * 16 / kRingWarps); }
 
 void count_message(gp_stats& s, int codec, uint64_t len) {
   const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
@@ -192,10 +196,9 @@ int gp_comm_create_emulated(int world, int device, uint64_t max_elems, gp_comm**
   c->nlocal = world;
   c->max_elems = std::max<uint64_t>(max_elems, 1);
   c->L = make_layout(world, c->max_elems);
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  // all p x G CTAs must be co-resident (1 x 512-thread CTA per SM)
-  c->G = std::max(1, std::min(16, sms / world));
+  // all p x G CTAs of the single launch must be co-resident
+  const int cap = sm_count(device) * ring_max_ctas_per_sm() / world;
+  c->G = std::max(1, std::min(16 * 16 / kRingWarps, cap));
   for (int i = 0; i < world; ++i) {
     int rc = alloc_inbox(c, i);
     if (rc) { for (int k = 0; k < i; ++k) cudaFree(c->inbox[k]); delete c; return rc; }
@@ -273,9 +276,8 @@ int gp_comm_connect_local(gp_comm* const* comms, int world) {
 int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   if (ctas > 0) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    const int cap = std::max(1, sms / c->nlocal);  // every CTA of the launch co-resident
+    // every CTA of one launch resident at once (emulated: all ranks' CTAs)
+    const int cap = std::max(1, sm_count(c->device) * ring_max_ctas_per_sm() / c->nlocal);
     c->G = std::min(ctas, cap);
   }
   if (timeout_s > 0) c->timeout_s = timeout_s;

@@ -28,6 +28,7 @@
 // push over NVSwitch (the bytes the ring would forward, one hop not p-1).
 // Emulation: with nlocal == p the same kernel runs all p ranks on one GPU
 // in one cooperative launch (CTA group = rank) for parity tests at p > #GPUs.
+#include <algorithm>
 #include <cstdlib>
 
 #include "codec.cuh"
@@ -521,7 +522,8 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
 }
 
 template <int C>
-__global__ void __launch_bounds__(kRingThreads) ring_allreduce_kernel(const __grid_constant__ RingParams P) {
+__global__ void __launch_bounds__(kRingThreads, 2048 / kRingThreads / 4 > 0 ? 2048 / kRingThreads / 4 : 1)
+    ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
   if (threadIdx.x == 0) s_seq = (uint32_t)(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)) + 1);
@@ -565,5 +567,17 @@ void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError
 }
 
 int ring_warps_per_cta() { return kWarps; }
+
+int ring_max_ctas_per_sm() {
+  int m = 1 << 30;
+  const void* fns[3] = {(const void*)ring_allreduce_kernel<kNone>, (const void*)ring_allreduce_kernel<kTrunc16>,
+                        (const void*)ring_allreduce_kernel<kQuant8>};
+  for (const void* f : fns) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, kRingThreads, 0);
+    m = std::min(m, std::max(b, 1));
+  }
+  return m;
+}
 
 }  // namespace gp

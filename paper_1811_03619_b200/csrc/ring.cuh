@@ -6,7 +6,10 @@
 
 namespace gp {
 
-constexpr int kRingThreads = 512;
+#ifndef PIPESGD_RING_THREADS
+#define PIPESGD_RING_THREADS 128
+#endif
+constexpr int kRingThreads = PIPESGD_RING_THREADS;
 constexpr int kRingWarps = kRingThreads / 32;
 constexpr uint32_t kMinChunk = 1024;   // elements per warp chunk; flags are sized for this
 constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of fp32)
@@ -72,5 +75,6 @@ __host__ __device__ inline void block_range(uint64_t n, int p, int b, uint64_t& 
 }
 
 void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError_t* err);
+int ring_max_ctas_per_sm();  // occupancy of the ring kernel (worst codec)
 
 }  // namespace gp

@@ -435,11 +435,12 @@ class RankEngine:
 
 # ----------------------------------------------------------------- clusters
 
-# SMs the ring kernel may occupy while the compute stream runs the next
-# iteration (the rest of the 148 stay free for forward/backward); the ring
-# reaches ~300-500 GB/s at 32 CTAs on 2xB200 (profiles/), far above what a
-# pipelined step needs to stay compute-bound.
-COMM_CTAS = 32
+# CTAs (128 threads each, 512 warps in total) the ring kernel may occupy
+# while the compute stream runs the next iteration; they share SMs with the
+# forward/backward kernels. The ring reaches ~300-530 GB/s at this budget on
+# 2xB200 (profiles/r01_ring_ctas_ab.log), far above what a pipelined step needs
+# to stay compute-bound.
+COMM_CTAS = 128
 
 
 def _make_transport(workers: int, timeout_s: float, max_elems: int, ctas: int = COMM_CTAS):
