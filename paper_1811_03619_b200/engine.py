@@ -534,3 +534,52 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
         real = [e for e in errors if not isinstance(e, threading.BrokenBarrierError)]
         raise (real or errors)[0]
     return results
+
+
+def run_process_worker(config: RunConfig, dataset, model, timeout_s: float = 30.0, batch_provider=None,
+                       grad_fn=None, trace: bool = True, fused: bool = True, comm_ctas: int = COMM_CTAS,
+                       group=None) -> WorkerResult:
+    """One rank of a multi-process run (one process per GPU under torchrun):
+    the analogue of the reference's run_tcp_worker (engine.py:621-646).
+    torch.distributed must be initialised; the rank's GPU is LOCAL_RANK.
+    Ranks exchange inbox IPC handles once over the process group, then the
+    ring moves gradients over NVLink only."""
+    import os
+
+    import torch.distributed as dist
+
+    from .transport import ProcessGroupTransport
+
+    if not dist.is_initialized():
+        raise ConfigError("run_process_worker needs torch.distributed initialised (torchrun)")
+    rank, workers = dist.get_rank(group), dist.get_world_size(group)
+    local = int(os.environ.get("LOCAL_RANK", rank % max(1, torch.cuda.device_count())))
+    torch.cuda.set_device(local)
+    if not isinstance(model, ModelSpec):
+        model = ModelSpec(model.kind, tuple(model.layer_dims))
+    ep = ProcessGroupTransport.endpoint(local, group=group, timeout_s=timeout_s,
+                                        max_elems=max(model.num_params, 1), ctas=comm_ctas)
+    dev = ep.device
+    shard = np.arange(rank % workers, dataset.features.shape[0], workers)
+    if batch_provider is None and grad_fn is None and config.batch_size > len(shard):
+        raise ConfigError(f"rank {rank}: batch size {config.batch_size} exceeds shard of {len(shard)} samples")
+    with torch.cuda.device(dev):
+        fm = FlatModel(SpecNet(model), dev, init_params(model, config.seed))
+        data = DeviceDataset(dataset, dev) if grad_fn is None else None
+        rng = np.random.default_rng([config.seed, rank])
+
+        def batch_fn(r, t):
+            idx = batch_provider(r, t) if batch_provider else \
+                shard[rng.choice(len(shard), size=config.batch_size, replace=False)]
+            return data.gather(idx)
+
+        eng = RankEngine(rank, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn, fused=fused)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group)
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(eng.cs)
+        eng.ms.wait_stream(eng.cs)
+        t0 = time.perf_counter()
+        eng.run(max(1, len(shard) // config.batch_size))
+        eng.cs.synchronize()
+        return eng.finish(start, time.perf_counter() - t0)

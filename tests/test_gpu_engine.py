@@ -149,3 +149,25 @@ def test_allreduce_overlaps_next_iteration_compute(P):
             c0, c1 = comp[t + 1]
             ov += min(a1, c1) > max(a0, c0)
     assert cand > 10 and ov >= cand * 0.5, (ov, cand)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_run_process_worker_under_torchrun_bit_exact():
+    """One process per GPU (torchrun, CUDA IPC inboxes): run_process_worker
+    with oracle gradients reproduces the oracle trajectory bit for bit."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tools", "process_worker_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert res and all(res.values()), res
