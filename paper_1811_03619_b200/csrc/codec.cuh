@@ -63,17 +63,22 @@ __device__ __forceinline__ Q8 q8_make(float s) {
   return q;
 }
 
-// One element -> int8 code (as int). x==0 (either sign) always yields 0.
+// One element -> int8 code (as int), branch-free (the ring is instruction-
+// bound on this): both exact residual tests are evaluated and selected.
+// Scale 0 (vmax tiny or 0): x/0 is +-inf in the reference -> +-127, and
+// 0/0 casts to 0. x == 0 (either sign) always yields 0.
 __device__ __forceinline__ int q8_encode(float x, const Q8& q) {
-  if (q.zero) return x > 0.f ? 127 : (x < 0.f ? -127 : 0);
   const float a = __fmul_rn(fabsf(x), q.pre);
   const float y = __fmul_rn(a, q.inv);
-  int k = (int)fminf(floorf(__fadd_rn(y, 0.5f)), 127.f);
-  if (k >= 1 && __fmaf_rn((float)k - 0.5f, q.ss, -a) > 0.f)
-    k -= 1;
-  else if (k < 127 && __fmaf_rn((float)k + 0.5f, q.ss, -a) <= 0.f)
-    k += 1;
-  return x < 0.f ? -k : k;
+  float k = fminf(floorf(__fadd_rn(y, 0.5f)), 127.f);
+  const float r_lo = __fmaf_rn(k - 0.5f, q.ss, -a);  // > 0 : k too large
+  const float r_hi = __fmaf_rn(k + 0.5f, q.ss, -a);  // <= 0: k too small
+  const bool dec = (k >= 1.f) & (r_lo > 0.f);
+  const bool inc = (k < 127.f) & (r_hi <= 0.f);
+  k = dec ? k - 1.f : (inc ? k + 1.f : k);
+  int c = q.zero ? 127 : (int)k;
+  c = (a == 0.f) ? 0 : c;
+  return (x < 0.f) ? -c : c;
 }
 __device__ __forceinline__ float q8_decode(int code, float s) { return __fmul_rn((float)code, s); }
 

@@ -95,9 +95,11 @@ int sm_count(int device) {
   return sms;
 }
 
-// Default CTA budget: 16 warps per SM on every SM (one 512-thread CTA, or
-// four 128-thread CTAs, per SM).
-int default_ctas(int device) { return std::max(1, sm_count(device) * 16 / kRingWarps); }
+// Default CTA budget: up to 16 warps per SM on every SM, never more CTAs
+// than can be resident at once (the quant8 rank barrier needs all of them).
+int default_ctas(int device) {
+  return std::max(1, sm_count(device) * std::min(16 / kRingWarps, ring_max_ctas_per_sm()));
+}
 
 void count_message(gp_stats& s, int codec, uint64_t len) {
   const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;

@@ -217,15 +217,22 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
 
 // Iterate this lane's groups of chunk c of block B in 1024-element batches;
 // all loads of a batch are issued before any of its stores.
+#ifndef PIPESGD_Q8_UNROLL
+#define PIPESGD_Q8_UNROLL 1
+#endif
 template <int C, typename L, typename S>
 __device__ __forceinline__ void for_groups(const RingParams& P, const Blk& B, uint32_t c, L&& load, S&& use) {
   constexpr int E = CodecT<C>::E;
-  constexpr int U = (int)kBatch / (32 * E);
+  // groups per lane per batch: 1024-element batches, except quant8 whose
+  // 16-element groups and encode temporaries would spill at the 128-register
+  // budget with two in flight
+  constexpr int U = C == kQuant8 ? PIPESGD_Q8_UNROLL : (int)kBatch / (32 * E);
+  constexpr uint64_t kB = 32ull * E * U;
   const int lane = lane_id();
   const uint64_t cbase = B.A + (uint64_t)c * P.chunk;
   const uint64_t lo = max(B.start, cbase);
   const uint64_t hi = min(B.start + B.len, cbase + P.chunk);
-  for (uint64_t b0 = cbase; b0 < hi; b0 += kBatch) {
+  for (uint64_t b0 = cbase; b0 < hi; b0 += kB) {
     using T = decltype(load(b0, lo, hi, 0, E));
     T v[U];
 #pragma unroll
@@ -359,6 +366,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         vmax = fabsf(q8_decode(q8_encode(own, q0), q0.s));
       }
       q = q8_make(q8_scale(vmax));
+      stamp(P, wid, lr, 16);
     }
     uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
     for (uint32_t c = grab(ctl, 1); c < B.nch; c = grab(ctl, 1)) {
@@ -440,7 +448,9 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                       });
       }
       float vmax;
+      if (s == 0) stamp(P, wid, lr, 15);  // (p = 2: slot 15 is free) pass A done
       if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
+      if (s == 0) stamp(P, wid, lr, 17);
       const Q8 q = q8_make(q8_scale(vmax));
       // pass B: encode the partial with the block scale and push it (any
       // warp may take any chunk: pass A's partials are visible GPU-wide
@@ -521,8 +531,11 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   stamp(P, wid, lr, 19);
 }
 
+#ifndef PIPESGD_RING_MINBLOCKS
+#define PIPESGD_RING_MINBLOCKS (2048 / kRingThreads / 4 > 0 ? 2048 / kRingThreads / 4 : 1)
+#endif
 template <int C>
-__global__ void __launch_bounds__(kRingThreads, 2048 / kRingThreads / 4 > 0 ? 2048 / kRingThreads / 4 : 1)
+__global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);

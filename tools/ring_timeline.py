@@ -54,7 +54,10 @@ for rep in range(a.reps):
     _lib.call("gp_comm_set_trace", ep._comm, None)
     t = tr.view(W, 20).cpu().numpy().astype(np.int64)
     t0 = t[:, 0][t[:, 0] > 0].min()
-    names = {1: "send0_done", 2: "s0_first_in", 3: "s0_done", 18: "ag_first_in", 19: "end"}
+    names = {1: "send0_done", 2: "s0_first_in", 3: "s0_done", 18: "ag_first_in", 19: "end",
+             16: "q8_bar0_out", 17: "q8_s0_bar_out"}
+    if p == 2:
+        names[15] = "q8_s0_passA_done"
     for s_ in range(1, p - 1):
         names[2 + 2 * s_] = f"s{s_}_first_in"
         names[3 + 2 * s_] = f"s{s_}_done"
