@@ -233,7 +233,8 @@ MODEL_NAMES = {"c1": ("C1 (configs[0]): MNIST-shaped MLP 784-500-500-10", "MLP 7
 def workload_config(args, n, N):
     title, model = MODEL_NAMES.get(args.model, (args.model, args.model))
     width = args.depth if args.mode == "pipe_sgd" else 1
-    return {"workload": f"{title}, {'Pipe-SGD' if args.mode == 'pipe_sgd' else 'D-Sync'} width {width}, "
+    scheme = {"pipe_sgd": "Pipe-SGD", "d_sync": "D-Sync", "ps_sync": "PS-Sync"}[args.mode]
+    return {"workload": f"{title}, {scheme} width {width}, "
                         f"{args.codec} ring compression",
             "model": model, "params": n, "global_batch": args.global_batch,
             "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
@@ -316,7 +317,7 @@ def our_arm(args, ws, rank, local):
         return max_over_ranks(ms, dev), list(eng.events)
 
     pipe = args.mode == "pipe_sgd"
-    step = eng.step if pipe else eng.step_sync
+    step = eng.step if pipe else (eng.ps_step if args.mode == "ps_sync" else eng.step_sync)
     with torch.cuda.device(dev), torch.cuda.stream(eng.cs):
         if pipe:
             eng.prime(1)
@@ -334,7 +335,7 @@ def our_arm(args, ws, rank, local):
         t += args.steps
         if pipe:
             eng.drain(t - 1)
-        else:
+        elif args.mode == "d_sync":
             eng.drain_sync()
         torch.cuda.synchronize(dev)
     ep._check_errors(n)

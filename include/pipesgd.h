@@ -14,6 +14,8 @@
  *                           (engine.py:333) and pipe re-compress of the sum (engine.py:407)
  *   gp_allreduce_emulated   the same ring with all p ranks on one device
  *                           (collective.py:77-139 driven like tests/helpers.py:10-29)
+ *   gp_gather_sum           collective.py:215-252 gather_to_root (+ the PS server's fold)
+ *   gp_broadcast            collective.py:255-280 broadcast_from_root
  *   gp_comm_create/connect  transport.py:150-177 InProcTransport(world).endpoint(r)
  *                           transport.py:192-305 TcpEndpoint mesh set-up
  *   gp_get_stats/reset      transport.py:52-61, :85-91, :105-107 TrafficStats
@@ -111,6 +113,19 @@ int gp_allreduce_ex(gp_comm* comm, const float* in, float* out, void* slot, floa
 int gp_allreduce_emulated_ex(gp_comm* comm, const float* const* ins, float* const* outs, void* const* slots,
                              float* const* slot_scales, uint64_t n, int codec, int flags, uint32_t iteration,
                              void* stream);
+/* Star collectives for the PS-Sync baseline (collective.py:215-280, engine.py:503-552):
+ * gp_gather_sum: on `root`, out = x_root + x_0 + x_1 + ... (rank order, src != root) —
+ *   the reference's gather_to_root — or, with zero_first, 0 + x_0 + x_1 + ... (the
+ *   parameter server's fold from its zero vector); other ranks' `out` is untouched.
+ * gp_broadcast: every rank's out = root's in (bit-exact). */
+int gp_gather_sum(gp_comm* comm, const float* in, float* out, uint64_t n, int root, int zero_first,
+                  uint32_t iteration, void* stream);
+int gp_broadcast(gp_comm* comm, const float* in, float* out, uint64_t n, int root, uint32_t iteration,
+                 void* stream);
+int gp_gather_sum_emulated(gp_comm* comm, const float* const* ins, float* const* outs, uint64_t n, int root,
+                           int zero_first, uint32_t iteration, void* stream);
+int gp_broadcast_emulated(gp_comm* comm, const float* const* ins, float* const* outs, uint64_t n, int root,
+                          uint32_t iteration, void* stream);
 int gp_comm_poll_error(gp_comm* comm, gp_error* out); /* call after the stream completed; clears */
 int gp_get_stats(gp_comm* comm, int rank, gp_stats* out);
 int gp_reset_stats(gp_comm* comm);

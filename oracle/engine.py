@@ -13,6 +13,10 @@ Restates, for parity runs of the GPU engine:
   * engine.py:379-448  width-K pipe loop: zero-primed slots, ring, whole-vector
                        re-compress of the sum (:407), consume t-K, drain K
   * engine.py:469-478  warm-up switch (sync epochs, drain, fresh pipe buffer)
+  * engine.py:503-552  ps_sync: workers send D(C(grad)) (codec NONE on the
+                       wire) to the server, which folds them in rank order from
+                       its zero vector (collective.py:236-251), takes one SGD
+                       step and broadcasts the parameters (:255-280)
 
 Instead of threads and queues the oracle evaluates the data dependencies
 directly: every rank's gradient for iteration t depends only on that rank's
@@ -31,7 +35,7 @@ import numpy as np
 from . import codec as C
 from .ring import ring_allreduce_all
 
-D_SYNC, PIPE_SGD = "d_sync", "pipe_sgd"
+D_SYNC, PIPE_SGD, PS_SYNC = "d_sync", "pipe_sgd", "ps_sync"
 
 
 # --------------------------------------------------------------------- data
@@ -262,7 +266,17 @@ def run_trajectory(p: int, cfg: Config, data: Blobs | None = None, net: Net | No
             w = update(w, slots.pop(tag), tag, tag + K)
         return w
 
-    if cfg.mode == D_SYNC:
+    def ps_phase(w):
+        for t in range(1, T + 1):
+            total = np.zeros(n, np.float32)
+            for g in local_step(t, w):   # collective.py:236-251: acc starts at the server's zeros
+                total = total + g
+            w = update(w, total, t, t)   # engine.py:542-545, then broadcast (bit-exact copy)
+        return w
+
+    if cfg.mode == PS_SYNC:
+        w = ps_phase(w)
+    elif cfg.mode == D_SYNC:
         w = sync_phase(1, T, w)
     elif cfg.mode == PIPE_SGD:
         warm = min(T, cfg.warmup_epochs * per_epoch)

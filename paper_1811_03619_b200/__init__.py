@@ -20,7 +20,13 @@ from .compression import (  # noqa: E402
     serialize_block,
     wire_size,
 )
-from .collective import partition_blocks, pipelined_allreduce, ring_allreduce  # noqa: E402
+from .collective import (  # noqa: E402
+    broadcast_from_root,
+    gather_to_root,
+    partition_blocks,
+    pipelined_allreduce,
+    ring_allreduce,
+)
 from .errors import (  # noqa: E402
     CodecError,
     CollectiveError,

@@ -26,6 +26,7 @@ EXPORTS = (
     "gp_comm_create", "gp_comm_create_emulated", "gp_comm_ipc_handle", "gp_comm_connect_ipc",
     "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_info", "gp_comm_destroy",
     "gp_allreduce", "gp_allreduce_ex", "gp_allreduce_emulated", "gp_allreduce_emulated_ex",
+    "gp_gather_sum", "gp_broadcast", "gp_gather_sum_emulated", "gp_broadcast_emulated",
     "gp_comm_poll_error", "gp_get_stats",
     "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update",
     "gp_calib_p2p_copy", "gp_calib_p2p_copy_ex", "gp_calib_pingpong", "gp_last_error_string", "gp_version",
@@ -60,6 +61,10 @@ _SIGS = {
     "gp_allreduce_ex": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _i, _i, _u32, _vp]),
     "gp_allreduce_emulated_ex": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                       ctypes.POINTER(_vp), _u64, _i, _i, _u32, _vp]),
+    "gp_gather_sum": (_i, [_vp, _vp, _vp, _u64, _i, _i, _u32, _vp]),
+    "gp_broadcast": (_i, [_vp, _vp, _vp, _u64, _i, _u32, _vp]),
+    "gp_gather_sum_emulated": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _u64, _i, _i, _u32, _vp]),
+    "gp_broadcast_emulated": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _u64, _i, _u32, _vp]),
     "gp_comm_poll_error": (_i, [_vp, ctypes.POINTER(GpError)]),
     "gp_get_stats": (_i, [_vp, _i, ctypes.POINTER(GpStats)]),
     "gp_reset_stats": (_i, [_vp]),

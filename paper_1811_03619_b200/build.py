@@ -13,7 +13,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["ring.cu", "comm.cu", "codec_kernels.cu", "calib.cu"]
+SOURCES = ["ring.cu", "star.cu", "comm.cu", "codec_kernels.cu", "calib.cu"]
 OUT = os.path.join(HERE, "libpipesgd.so")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

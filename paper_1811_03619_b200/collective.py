@@ -104,3 +104,50 @@ def pipelined_allreduce(local, rank: int, p: int, endpoint: GpuEndpoint, codec: 
     The fused kernel streams each ring block in chunks, so the transfer of
     chunk c overlaps the decode/add/encode of chunk c-1 by construction."""
     return ring_allreduce(local, rank, p, endpoint, codec, iteration)
+
+
+# ------------------------------------------------------------------ star
+
+def gather_to_root(local, root: int, rank: int, p: int, endpoint: GpuEndpoint, iteration: int = 0):
+    """Root returns the elementwise sum local_root + x_0 + x_1 + ... in rank
+    order (src != root), others return None (collective.py:215-252)."""
+    _check_rank_args(local, rank, p, endpoint)
+    as_numpy = not isinstance(local, torch.Tensor)
+    dev = endpoint.device
+    with torch.cuda.device(dev):
+        x = _device_input(local, dev)
+        out = torch.empty_like(x) if rank == root else None
+        s = torch.cuda.current_stream(dev)
+        endpoint._star(x, out, x.numel(), root, 0, False, iteration, s)
+        endpoint_wait(endpoint, x.numel(), s)
+    if out is None:
+        return None
+    return out.cpu().numpy() if as_numpy else out
+
+
+def broadcast_from_root(value, root: int, rank: int, p: int, endpoint: GpuEndpoint, iteration: int = 0):
+    """Bit-exact copy of the root's vector on every rank (collective.py:255-280).
+    Non-roots pass None; the length travels first as one bit-copied element."""
+    if endpoint.rank != rank or endpoint.world_size != p:
+        raise CollectiveError("endpoint does not match caller's rank/size")
+    if rank == root and value is None:
+        raise CollectiveError("broadcast root has no value")
+    as_numpy = rank == root and not isinstance(value, torch.Tensor)
+    dev = endpoint.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream(dev)
+        hdr = torch.zeros(4, dtype=torch.int32, device=dev)
+        if rank == root:
+            x = _device_input(value, dev)
+            hdr[0] = x.numel()
+        got = torch.empty_like(hdr)
+        endpoint._star(hdr.view(torch.float32), got.view(torch.float32), 4, root, 1, False, iteration, s)
+        endpoint_wait(endpoint, 4, s)
+        n = int(got[0].item())
+        if rank != root:
+            x = torch.empty(n, dtype=torch.float32, device=dev)
+            as_numpy = not isinstance(value, torch.Tensor) if value is not None else True
+        out = torch.empty_like(x)
+        endpoint._star(x, out, n, root, 1, False, iteration, s)
+        endpoint_wait(endpoint, n, s)
+    return out.cpu().numpy() if as_numpy else out

@@ -434,6 +434,80 @@ int gp_allreduce_emulated_ex(gp_comm* c, const float* const* ins, float* const* 
   return launch(c, ins, outs, slots, slot_scales, n, codec, flags, iteration, static_cast<cudaStream_t>(stream));
 }
 
+// Reference accounting for the star: gather sends one n-element NONE message
+// from every non-root rank (collective.py:227-233); broadcast sends one to
+// every non-root rank from the root (:265-269).
+static int star(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int root, int mode,
+                int zero_first, cudaStream_t st) {
+  if (root < 0 || root >= c->world) return fail(GP_ERR_ARG, "root outside the communicator");
+  if (n > c->max_elems) return fail(GP_ERR_ARG, "vector exceeds communicator capacity");
+  StarLaunch S{};
+  S.L = c->L;
+  S.n = n;
+  S.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
+  S.p = c->world;
+  S.root = root;
+  S.mode = mode;
+  S.zero_first = zero_first;
+  S.ctas = std::max(1, c->G / 4);
+  S.nlocal = c->nlocal;
+  for (int i = 0; i < c->nlocal; ++i) {
+    const int r = c->nlocal == 1 ? c->rank : i;
+    if (n && !ins[i]) return fail(GP_ERR_ARG, "null buffer");
+    const bool needs_out = mode == 1 || r == root;
+    if (n && needs_out && !outs[i]) return fail(GP_ERR_ARG, "null output");
+    if (n && (misaligned(ins[i]) || (outs[i] && misaligned(outs[i]))))
+      return fail(GP_ERR_ARG, "buffers must be 16-byte aligned");
+    S.ins[i] = ins[i];
+    S.outs[i] = outs[i];
+    S.inboxes[i] = c->inbox[i];
+    S.ranks[i] = r;
+  }
+  for (int q = 0; q < c->world; ++q) S.peers[q] = c->peer[q];
+  cudaError_t e = launch_star(S, st);
+  if (e != cudaSuccess) return cuda_fail(e, "star kernel launch");
+  ++c->seq;
+  for (int i = 0; i < c->nlocal; ++i) {
+    const int r = c->nlocal == 1 ? c->rank : i;
+    if (mode == 0 && r != root) count_message(c->stats[i], GP_CODEC_NONE, n);
+    if (mode == 1 && r == root)
+      for (int q = 0; q < c->world - 1; ++q) count_message(c->stats[i], GP_CODEC_NONE, n);
+  }
+  return GP_OK;
+}
+
+int gp_gather_sum(gp_comm* c, const float* in, float* out, uint64_t n, int root, int zero_first,
+                  uint32_t iteration, void* stream) {
+  (void)iteration;
+  if (!c || c->nlocal != 1 || !c->connected) return fail(GP_ERR_STATE, "not a connected per-rank communicator");
+  DeviceGuard g(c->device);
+  return star(c, &in, &out, n, root, 0, zero_first, static_cast<cudaStream_t>(stream));
+}
+
+int gp_broadcast(gp_comm* c, const float* in, float* out, uint64_t n, int root, uint32_t iteration,
+                 void* stream) {
+  (void)iteration;
+  if (!c || c->nlocal != 1 || !c->connected) return fail(GP_ERR_STATE, "not a connected per-rank communicator");
+  DeviceGuard g(c->device);
+  return star(c, &in, &out, n, root, 1, 0, static_cast<cudaStream_t>(stream));
+}
+
+int gp_gather_sum_emulated(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int root,
+                           int zero_first, uint32_t iteration, void* stream) {
+  (void)iteration;
+  if (!c || (c->nlocal == 1 && c->world > 1)) return fail(GP_ERR_STATE, "not an emulated communicator");
+  DeviceGuard g(c->device);
+  return star(c, ins, outs, n, root, 0, zero_first, static_cast<cudaStream_t>(stream));
+}
+
+int gp_broadcast_emulated(gp_comm* c, const float* const* ins, float* const* outs, uint64_t n, int root,
+                          uint32_t iteration, void* stream) {
+  (void)iteration;
+  if (!c || (c->nlocal == 1 && c->world > 1)) return fail(GP_ERR_STATE, "not an emulated communicator");
+  DeviceGuard g(c->device);
+  return star(c, ins, outs, n, root, 1, 0, static_cast<cudaStream_t>(stream));
+}
+
 int gp_comm_poll_error(gp_comm* c, gp_error* out) {
   if (!c || !out) return fail(GP_ERR_ARG, "null argument");
   DeviceGuard g(c->device);

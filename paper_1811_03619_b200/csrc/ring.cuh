@@ -75,6 +75,19 @@ __host__ __device__ inline void block_range(uint64_t n, int p, int b, uint64_t& 
 }
 
 void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError_t* err);
+
+// Star collectives (star.cu): gather-sum to a root / broadcast from a root.
+struct StarLaunch {
+  Layout L;
+  uint64_t n, timeout_ns;
+  int p, root, mode, zero_first, ctas, nlocal;
+  const float* ins[kMaxRanks];
+  float* outs[kMaxRanks];
+  uint8_t* inboxes[kMaxRanks];
+  uint8_t* peers[kMaxRanks];
+  int ranks[kMaxRanks];
+};
+cudaError_t launch_star(const StarLaunch& S, cudaStream_t stream);
 int ring_max_ctas_per_sm();  // occupancy of the ring kernel (worst codec)
 
 }  // namespace gp

@@ -85,8 +85,6 @@ class RunConfig:
     def __post_init__(self) -> None:
         if self.mode not in MODES:
             raise ConfigError(f"unknown mode {self.mode!r}")
-        if self.mode == MODE_PS_SYNC:
-            raise ConfigError("ps_sync (parameter server) is not on the GPU hot path; use d_sync or pipe_sgd")
         if self.iterations < 1:
             raise ConfigError("need at least one iteration")
         if self.learning_rate <= 0:
@@ -390,6 +388,47 @@ class RankEngine:
             self.step(t)
         self.drain(t1)
 
+    def ps_step(self, t: int) -> None:
+        """PS-Sync (engine.py:503-552) with the server role co-located on rank 0:
+        local D(C(grad)) -> gather, the server folding 0 + x_0 + ... + x_{p-1}
+        in rank order (collective.py:236-251) -> the server's SGD step with the
+        mean (engine.py:542-545) -> broadcast of the parameters (:546-549).
+        Not pipelined: every stage is on the compute stream."""
+        i = t % self.K
+        if self.fused:
+            self.fm.use_grad_buffer(i)
+        e0 = self._ev(self.cs) if self.tracing else None
+        if self.grad_fn is not None:
+            self.cs.synchronize()
+            loss, g = self.grad_fn(self.rank, t, self.fm.params)
+            self.fm.grads.copy_(torch.as_tensor(np.asarray(g, np.float32)).to(self.dev))
+            self.losses[t].fill_(float(loss))
+        else:
+            x, y = self.batch_fn(self.rank, t)
+            self.losses[t].copy_(self.fm.loss_and_grad(x, y))
+        e1 = self._ev(self.cs) if self.tracing else None
+        roundtrip_async(self.fm.grads, self.cfg.codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+        e2 = self._ev(self.cs) if self.tracing else None
+        root = 0
+        self.ep._star(self.local[i], self.summed if self.rank == root else None, self.n, root, 0, True, t, self.cs)
+        if self.rank == root:
+            lr = float(np.float32(self._lr(t)))
+            _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(Codec.NONE),
+                      self.summed.data_ptr(), self.local_status[i].scale_view.data_ptr(), self.n, lr, self.world,
+                      self.cs.cuda_stream)
+        self.ep._star(self.fm.params, self.fm.params, self.n, root, 1, False, t, self.cs)
+        if self.tracing:
+            e3 = self._ev(self.cs)
+            self._rec(t, STAGE_BACKWARD, e0, e1)
+            self._rec(t, STAGE_COMPRESS, e1, e2)
+            self._rec(t, STAGE_ALLREDUCE, e2, e3)
+        self.updates_seen += 1
+        if self.updates_seen <= self.cfg.snapshot_first:
+            self.early_params.append((t, self.fm.params.clone()))
+        if self.cfg.eval_interval and self.rank == 0 and t % self.cfg.eval_interval == 0:
+            self.eval_points.append((t, self.fm.params.clone()))
+        self._mark(t)
+
     def _mark(self, t):
         e = torch.cuda.Event(enable_timing=True)
         e.record(self.cs)
@@ -402,6 +441,9 @@ class RankEngine:
         with torch.cuda.device(self.dev), torch.cuda.stream(self.cs):
             if cfg.mode == MODE_D_SYNC:
                 self.sync_phase(1, cfg.iterations)
+            elif cfg.mode == MODE_PS_SYNC:
+                for t in range(1, cfg.iterations + 1):
+                    self.ps_step(t)
             else:
                 warm = min(cfg.iterations, cfg.warmup_epochs * iters_per_epoch)
                 if warm > 0:
@@ -426,11 +468,15 @@ class RankEngine:
                                     int(start_ev.elapsed_time(e1) * 1e6), consumed))
         trace.sort(key=lambda e: (e.start_ns, e.iteration))
         dev_s = start_ev.elapsed_time(self.end) / 1e3
+        stats = self.ep.stats.snapshot()
+        if self.cfg.mode == MODE_PS_SYNC:  # the worker role's traffic (engine.py:513-519): one gather message
+            T, pb = self.cfg.iterations, 4 * self.n
+            stats = TrafficStats(T, T * pb, T * (pb + 20))
         return WorkerResult(
             rank=self.rank, params=self.fm.params.cpu().numpy(), trace=trace, metrics=metrics,
             eval_points=[(t, p.cpu().numpy()) for t, p in self.eval_points],
             early_params=[(t, p.cpu().numpy()) for t, p in self.early_params],
-            stats=self.ep.stats.snapshot(), train_seconds=train_seconds, device_seconds=dev_s)
+            stats=stats, train_seconds=train_seconds, device_seconds=dev_s)
 
 
 # ----------------------------------------------------------------- clusters
@@ -533,6 +579,15 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
     if errors:
         real = [e for e in errors if not isinstance(e, threading.BrokenBarrierError)]
         raise (real or errors)[0]
+    if config.mode == MODE_PS_SYNC:
+        # the reference returns the server's result last (engine.py:581, :600):
+        # here the server role lives on rank 0, so its state is rank 0's
+        import dataclasses
+        T, pb = config.iterations, 4 * n
+        server = dataclasses.replace(results[0], rank=workers, is_server=True, metrics=[], eval_points=[],
+                                     early_params=[],
+                                     stats=TrafficStats(T * workers, T * workers * pb, T * workers * (pb + 20)))
+        results = results + [server]
     return results
 
 

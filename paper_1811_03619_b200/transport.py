@@ -118,6 +118,18 @@ class GpuEndpoint:
         _lib.call("gp_allreduce_ex", self._comm, x.data_ptr(), _ptr(out), _ptr(slot), _ptr(slot_scale),
                   x.numel(), int(codec), int(flags), int(iteration) & 0xFFFFFFFF, stream.cuda_stream)
 
+    def _star(self, x: torch.Tensor, out: torch.Tensor | None, n: int, root: int, mode: int, zero_first: bool,
+              iteration: int, stream: torch.cuda.Stream) -> None:
+        """Star collective (mode 0 gather-sum to root, 1 broadcast from root)."""
+        if self._poisoned:
+            raise CollectiveError(f"endpoint {self.rank} is unusable after an earlier failure: {self._poisoned}")
+        if mode == 0:
+            _lib.call("gp_gather_sum", self._comm, x.data_ptr(), _ptr(out), n, int(root), int(zero_first),
+                      int(iteration) & 0xFFFFFFFF, stream.cuda_stream)
+        else:
+            _lib.call("gp_broadcast", self._comm, x.data_ptr(), _ptr(out), n, int(root),
+                      int(iteration) & 0xFFFFFFFF, stream.cuda_stream)
+
     def _check_errors(self, n: int) -> None:
         """After the launching stream completed: raise what the device latched."""
         e = _lib.GpError()
@@ -212,6 +224,10 @@ class EmulatedEndpoint(GpuEndpoint):
     def _launch(self, x, out, codec, iteration, stream, flags=0, slot=None, slot_scale=None):
         self._gen = self._transport._arrive(self.rank, x, out, codec, iteration, stream, flags, slot, slot_scale)
 
+    def _star(self, x, out, n, root, mode, zero_first, iteration, stream):
+        self._gen = self._transport._arrive(self.rank, x, out, -1 - mode, iteration, stream,
+                                            (int(root) << 1) | int(bool(zero_first)), None, None, n=n)
+
     def _check_errors(self, n: int) -> None:
         self._transport._finish(getattr(self, "_gen", None))
 
@@ -247,14 +263,18 @@ class EmulatedTransport:
     def endpoint(self, rank: int) -> EmulatedEndpoint:
         return self._eps[rank]
 
-    def _arrive(self, rank, x, out, codec, iteration, stream, flags=0, slot=None, slot_scale=None) -> _Generation:
+    def _arrive(self, rank, x, out, codec, iteration, stream, flags=0, slot=None, slot_scale=None,
+                n=None) -> _Generation:
+        """codec >= 0: ring allreduce; -1: gather-sum, -2: broadcast (flags =
+        root << 1 | zero_first)."""
         ev = torch.cuda.Event()
         ev.record(stream)
         with self._cv:
             gen = self._cur
             if rank in gen.slots:
-                raise CollectiveError(f"rank {rank} entered the same allreduce twice")
-            gen.slots[rank] = (x, out, int(codec), int(iteration), x.numel(), ev, int(flags), slot, slot_scale)
+                raise CollectiveError(f"rank {rank} entered the same collective twice")
+            gen.slots[rank] = (x, out, int(codec), int(iteration), x.numel() if n is None else int(n), ev,
+                               int(flags), slot, slot_scale)
             if len(gen.slots) == self.world_size:
                 self._launch_all(gen)
                 self._cur = _Generation()
@@ -288,8 +308,15 @@ class EmulatedTransport:
             for t in (a[0], a[1], a[7], a[8]):
                 if t is not None:
                     t.record_stream(self._stream)
-        _lib.call("gp_allreduce_emulated_ex", self._comm, ins, outs, slots, scales, gen.n, args[0][2], args[0][6],
-                  args[0][3] & 0xFFFFFFFF, self._stream.cuda_stream)
+        op, fl, it = args[0][2], args[0][6], args[0][3] & 0xFFFFFFFF
+        if op >= 0:
+            _lib.call("gp_allreduce_emulated_ex", self._comm, ins, outs, slots, scales, gen.n, op, fl, it,
+                      self._stream.cuda_stream)
+        elif op == -1:
+            _lib.call("gp_gather_sum_emulated", self._comm, ins, outs, gen.n, fl >> 1, fl & 1, it,
+                      self._stream.cuda_stream)
+        else:
+            _lib.call("gp_broadcast_emulated", self._comm, ins, outs, gen.n, fl >> 1, it, self._stream.cuda_stream)
         gen.done = torch.cuda.Event()
         gen.done.record(self._stream)
         gen.slots = {}

@@ -14,4 +14,8 @@ ENGINE_CASES = [
     ("mlp_ds_q8_p2", "mlp", "d_sync", 2, 2, 6, 2, 0, 0.05, 25, 0),
     ("mlp_ps_t16_p4_warm", "mlp", "pipe_sgd", 1, 4, 12, 2, 1, 0.05, 32, 0),
     ("log_ps_q8_p1", "log", "pipe_sgd", 2, 1, 7, 2, 0, 0.1, 16, 0),
+    ("log_pss_none_p1", "log", "ps_sync", 0, 1, 6, 2, 0, 0.2, 16, 0),
+    ("mlp_pss_t16_p2", "mlp", "ps_sync", 1, 2, 6, 2, 0, 0.05, 25, 0),
+    ("mlp_pss_q8_p4", "mlp", "ps_sync", 2, 4, 6, 2, 0, 0.05, 25, 3),
+    ("log_pss_none_p4", "log", "ps_sync", 0, 4, 7, 2, 0, 0.1, 16, 0),
 ]

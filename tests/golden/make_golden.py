@@ -170,7 +170,7 @@ def make_engine():
                         depth=K, batch_size=bs, warmup_epochs=warm, seed=7,
                         lr_decay_every=dec, lr_decay_factor=0.5)
         res = run_inproc_cluster(p, cfg, data, models[m])
-        for r in res[1:]:
+        for r in res[1:]:  # workers and, in ps_sync, the server (last result)
             assert r.params.tobytes() == res[0].params.tobytes()
         out[name] = res[0].params
         out[name + "_loss"] = np.array([x[2] for x in res[0].metrics])

@@ -171,3 +171,40 @@ def test_run_process_worker_under_torchrun_bit_exact():
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert res and all(res.values()), res
+
+
+def test_ps_sync_server_is_last_and_matches_workers(P, blobs):
+    """test_engine.py:160-167: the server result comes last, params equal."""
+    from paper_1811_03619_b200.engine import RunConfig, run_inproc_cluster
+    from paper_1811_03619_b200.models import ModelSpec
+    cfg = RunConfig(mode="ps_sync", iterations=3, batch_size=16, seed=1)
+    res = run_inproc_cluster(2, cfg, blobs, ModelSpec("logistic", (8, 3)))
+    assert [r.is_server for r in res] == [False, False, True]
+    assert_bits_equal(res[0].params, res[2].params, "server vs worker")
+    assert res[0].stats.messages == 3 and res[2].stats.messages == 6
+
+
+def test_star_collectives_match_reference_semantics(P):
+    """collective.py:215-280: gather folds local_root + others in rank order;
+    broadcast is bit-exact (test_collective.py:178-221)."""
+    from helpers import run_ranks
+    from paper_1811_03619_b200.collective import broadcast_from_root, gather_to_root
+    p = 4
+    tr = P.EmulatedTransport(p, timeout_s=30.0, max_elems=1 << 20)
+    try:
+        g = np.random.default_rng(5)
+        ins = [(g.normal(0, 1, 1000_003) * 10.0 ** g.integers(-3, 3)).astype(np.float32) for _ in range(p)]
+        for root in (0, 2):
+            outs = run_ranks(tr, lambda r, ep: gather_to_root(ins[r], root, r, p, ep))
+            want = ins[root].copy()
+            for s in range(p):
+                if s != root:
+                    want = want + ins[s]
+            assert_bits_equal(outs[root], want, f"gather root {root}")
+            assert all(o is None for r, o in enumerate(outs) if r != root)
+        value = g.normal(0, 1, 1_000_000).astype(np.float32)
+        outs = run_ranks(tr, lambda r, ep: broadcast_from_root(value if r == 3 else None, 3, r, p, ep))
+        for o in outs:
+            assert o.tobytes() == value.tobytes()
+    finally:
+        tr.close()
