@@ -388,6 +388,83 @@ class RankEngine:
             self.step(t)
         self.drain(t1)
 
+    # --------------------------------------------------------- CUDA graphs
+    def capture_graphs(self, batch) -> None:
+        """Capture the steady-state pipelined iteration as 2K CUDA graphs.
+
+        For parity i = t % K: compute graph i (compute stream) = consume slot i
+        + forward/backward of `batch` into gradient buffer i; comm graph i
+        (comm stream) = the fused ring from gradient buffer i into slot i.
+        Replays are linked by events between the streams, so iteration t's
+        ring still overlaps iteration t+1's compute. The ring kernel reads its
+        call sequence number on the device, so every replay is a new call.
+        Requirements: pipe mode, fused path, real GPU transport, constant
+        learning rate, static batch tensors (refilled in place by the caller)."""
+        cfg = self.cfg
+        if not self.fused or cfg.mode != MODE_PIPE_SGD or cfg.lr_decay_every > 0 or self.grad_fn is not None:
+            raise ConfigError("graph mode needs fused pipe_sgd with a constant learning rate and a model")
+        if type(self.ep).__name__ == "EmulatedEndpoint":
+            raise ConfigError("graph mode needs one GPU per rank (the emulated ring rendezvouses on the host)")
+        x, y = batch
+        lr = float(np.float32(cfg.learning_rate))
+        self.static_loss = [torch.zeros((), dtype=torch.float32, device=self.dev) for _ in range(self.K)]
+        self.g_compute, self.g_comm = [], []
+        self.ev_agg = [torch.cuda.Event() for _ in range(self.K)]
+        torch.cuda.synchronize(self.dev)
+        for i in range(self.K):
+            slot = self.slots[i]
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
+                _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
+                          slot.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+                self.fm.use_grad_buffer(i)
+                self.static_loss[i].copy_(self.fm.loss_and_grad(x, y))
+            gm = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gm, stream=self.ms, capture_error_mode="thread_local"):
+                g = self.fm.grad_bufs[i]
+                if self.world > 1:
+                    allreduce_into(g, self.summed, self.ep, cfg.codec, 0, self.ms, precompress=True,
+                                   slot=slot.payload, slot_scale=slot.status.scale_view)
+                else:
+                    encode_async(g, cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
+            self.g_compute.append(gc)
+            self.g_comm.append(gm)
+        self.graph_ready_tag = {}
+
+    def step_graph(self, t: int) -> None:
+        """One pipelined iteration by graph replay (after prime / eager warm-up)."""
+        i = t % self.K
+        prev = self.graph_ready_tag.pop(i, None)
+        if prev is not None:
+            self.cs.wait_event(self.ev_agg[i])
+        else:  # slot i still holds the eager pipeline's tag t-K: wait for it
+            self.buffer.take(t - self.K, self.cs)
+        e0 = self._ev(self.cs) if self.tracing else None
+        self.g_compute[i].replay()
+        self.losses[t].copy_(self.static_loss[i])
+        self.ev_local[i].record(self.cs)
+        self.ms.wait_event(self.ev_local[i])
+        e1 = self._ev(self.ms) if self.tracing else None
+        with torch.cuda.stream(self.ms):
+            self.g_comm[i].replay()
+        self.ev_agg[i].record(self.ms)
+        if self.tracing:
+            self._rec(t, STAGE_BACKWARD, e0, self._ev(self.cs))
+            e2 = self._ev(self.ms)
+            self._rec(t, STAGE_ALLREDUCE, e1, e2)
+            self._rec(t, "ring" if self.world > 1 else "recompress", e1, e2)
+        self.graph_ready_tag[i] = t
+        self._mark(t)
+
+    def drain_graph(self, t1: int) -> None:
+        lr = float(np.float32(self.cfg.learning_rate))
+        for tag in range(t1 - self.K + 1, t1 + 1):
+            i = tag % self.K
+            self.cs.wait_event(self.ev_agg[i])
+            slot = self.slots[i]
+            _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
+                      slot.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+
     def ps_step(self, t: int) -> None:
         """PS-Sync (engine.py:503-552) with the server role co-located on rank 0:
         local D(C(grad)) -> gather, the server folding 0 + x_0 + ... + x_{p-1}

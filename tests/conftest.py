@@ -23,3 +23,10 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "multigpu" in item.keywords and "gpu" not in item.keywords:
             item.add_marker(pytest.mark.gpu)
+
+
+@pytest.fixture(scope="session")
+def P():
+    """The product package (GPU tests)."""
+    import paper_1811_03619_b200 as pkg
+    return pkg

@@ -1,0 +1,65 @@
+"""CUDA-graph replay of the pipelined step (RankEngine.capture_graphs /
+step_graph) computes exactly what the eager engine computes: same weights,
+bit for bit, after warm-up + graph steps + drain, for p = 1 and (with two
+GPUs) p = 2 over NVLink, every codec."""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import assert_bits_equal, run_ranks
+
+pytestmark = pytest.mark.gpu
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def train(P, p, codec, graphs, T=12, W=3):
+    from paper_1811_03619_b200.engine import RankEngine, RunConfig
+    from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
+    spec = ModelSpec("mlp", (64, 128, 10))
+    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=spec.num_params, ctas=64)
+
+    def op(r, ep):
+        dev = torch.device("cuda", r)
+        with torch.cuda.device(dev):
+            fm = FlatModel(SpecNet(spec), dev, init_params(spec, 1))
+            g = torch.Generator(device="cpu").manual_seed(10 + r)
+            x = torch.randn(32, 64, generator=g).to(dev)
+            y = torch.randint(0, 10, (32,), generator=g).to(dev)
+            cfg = RunConfig(mode="pipe_sgd", iterations=T + 2, learning_rate=0.05, codec=codec, batch_size=32)
+            eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False)
+            with torch.cuda.stream(eng.cs):
+                eng.prime(1)
+                for t in range(1, W + 1):
+                    eng.step(t)
+                if graphs:
+                    eng.capture_graphs((x, y))
+                    for t in range(W + 1, T + 1):
+                        eng.step_graph(t)
+                    eng.drain_graph(T)
+                else:
+                    for t in range(W + 1, T + 1):
+                        eng.step(t)
+                    eng.drain(T)
+            torch.cuda.synchronize(dev)
+            ep._check_errors(fm.num_params)
+            return fm.params.cpu().numpy(), eng.losses[1:T + 1].cpu().numpy()
+
+    try:
+        return run_ranks(tr, op)
+    finally:
+        tr.close()
+
+
+@pytest.mark.parametrize("codec", [0, 1, 2])
+@pytest.mark.parametrize("p", [1, 2])
+def test_graph_replay_matches_eager(P, p, codec):
+    if p > NGPU:
+        pytest.skip("needs more GPUs")
+    eager = train(P, p, codec, graphs=False)
+    graph = train(P, p, codec, graphs=True)
+    for r in range(p):
+        assert_bits_equal(graph[r][0], eager[r][0], f"p={p} codec={codec} rank {r} weights")
+        np.testing.assert_array_equal(graph[r][1], eager[r][1])
+    for r in range(1, p):
+        assert_bits_equal(graph[r][0], graph[0][0], "replicas")
