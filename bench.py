@@ -260,15 +260,16 @@ def our_arm(args, ws, rank, local):
     dev = torch.device("cuda", local)
     N = ws
     torch.backends.cudnn.benchmark = True
-    if N > 1:
-        ep = ProcessGroupTransport.endpoint(local, max_elems=1 << 26, ctas=args.ctas, timeout_s=60.0)
-    else:
-        tr = GpuTransport(1, max_elems=1 << 10, ctas=args.ctas)
-        ep = tr.endpoint(0)
     torch.manual_seed(0)  # identical replicas on every rank
     mod, in_shape, classes = build_torch_model(args.model)
     fm = FlatModel(mod, dev)
     n = fm.num_params
+    cap = max(n, 1 << 26) if N > 1 else (n if args.mode == "ps_sync" else 1 << 10)
+    if N > 1:
+        ep = ProcessGroupTransport.endpoint(local, max_elems=cap, ctas=args.ctas, timeout_s=60.0)
+    else:
+        tr = GpuTransport(1, max_elems=cap, ctas=args.ctas)
+        ep = tr.endpoint(0)
     B = args.global_batch // N
     total_steps = 2 * (args.warmup + args.steps) + 8
     cfg = RunConfig(mode=args.mode, iterations=total_steps, learning_rate=0.01, codec=args.codec,
@@ -404,7 +405,8 @@ def our_arm(args, ws, rank, local):
         kernels[k] = {"in_pipeline_avg_ms": avg.get(k), "isolated_avg_ms": iso.get(k)}
         if k in algo:
             kernels[k]["algorithmic_bytes"] = algo[k]
-            kernels[k]["isolated_hbm_gbs"] = algo[k] / (iso[k] * 1e-3) / 1e9
+            if iso.get(k):
+                kernels[k]["isolated_hbm_gbs"] = algo[k] / (iso[k] * 1e-3) / 1e9
             if k in avg:
                 kernels[k]["in_pipeline_hbm_gbs"] = algo[k] / (avg[k] * 1e-3) / 1e9
     traffic = ncu_traffic()
@@ -412,21 +414,21 @@ def our_arm(args, ws, rank, local):
         kr = kernels["ring"]
         kr["wire_bytes"] = wire
         kr["isolated_nvlink_gbs"] = wire / (iso["ring"] * 1e-3) / 1e9
-        kr["in_pipeline_nvlink_gbs"] = wire / (avg["ring"] * 1e-3) / 1e9
+        kr["in_pipeline_nvlink_gbs"] = wire / (avg["ring"] * 1e-3) / 1e9 if avg.get("ring") else None
         roof = {"kernel": "ring_allreduce_kernel<%s> (fused decode+add+encode+NVLink push)" % args.codec,
                 "bound": "nvlink", "achieved": kr["isolated_nvlink_gbs"], "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": kr["isolated_nvlink_gbs"] / NVLINK_PEAK_GBS,
                 "traffic": None,
                 "measured": "kernel alone on the step's gradient (L2 flushed, ranks barrier-aligned, median of "
                             "launches); in the pipeline the same launch also waits for slower ranks: "
-                            f"{kr['in_pipeline_nvlink_gbs']:.1f} GB/s",
+                            f"{kr['in_pipeline_nvlink_gbs'] or 0:.1f} GB/s",
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (MEASURED_PEAKS.json has "
                                "no NVLink entry); this pool's bidirectional push ceiling measured by "
                                "gp_calib_p2p_copy is ~690-707 GB/s",
                 "algorithmic_bytes_per_launch": wire}
     else:
         copy_gbs = 8 * n / (iso["copy_4n"] * 1e-3) / 1e9
-        dom = max([k for k in ("update", "compress", "recompress") if k in kernels],
+        dom = max([k for k in ("update", "compress", "recompress") if k in kernels and iso.get(k)],
                   key=lambda k: avg.get(k, 0.0))
         name = {"update": "consume_update_kernel", "compress": "roundtrip_kernel",
                 "recompress": "encode_kernel"}[dom]

@@ -151,7 +151,9 @@ __device__ void star_body(const StarParams& P) {
     }
     return;
   }
-  // gather at the root: fold the sources in the reference's order
+  // gather at the root: fold the sources in the reference's order, one
+  // streaming pass per source over the chunk (8 x 16 B loads in flight per
+  // lane, remote sources read over NVLink, the running sum kept in `out`)
   for (uint32_t c = star_grab(ctl, 1); c < nch; c = star_grab(ctl, 1)) {
     int ok = 1;
     if (lane == 0)
@@ -160,34 +162,53 @@ __device__ void star_body(const StarParams& P) {
     __syncwarp();
     if (!__shfl_sync(0xffffffffu, ok, 0)) return;
     const uint64_t b = (uint64_t)c * P.chunk, e = min(n, b + P.chunk);
-    for (uint64_t g = b + 4ull * lane; g < e; g += 4ull * 32) {
-      float acc[4];
-      const int m = (int)(e - g < 4 ? e - g : 4);
-      auto load4 = [&](const float* base, float* v) {
-        if (m == 4) {
-          const float4 t = __ldcg(reinterpret_cast<const float4*>(base + g));
-          v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-        } else {
-          for (int k = 0; k < 4; ++k) v[k] = k < m ? __ldcg(base + g + k) : 0.f;
-        }
-      };
-      if (P.zero_first) {
-        acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-      } else {
-        load4(R.in, acc);
-      }
-      for (int s = 0; s < P.p; ++s) {
-        if (!P.zero_first && s == R.rank) continue;
-        float v[4];
-        load4(s == R.rank ? R.in : staged(R.peer[s], P.L), v);
+    // source order: [root, others ascending] (gather_to_root) or
+    // [zero, 0, 1, ..., p-1] (the parameter server's zero vector first)
+    const int nsrc = P.zero_first ? P.p : P.p;
+    for (int k = 0; k < nsrc; ++k) {
+      int s;
+      if (P.zero_first) s = k;
+      else s = (k == 0) ? R.rank : (k <= R.rank ? k - 1 : k);
+      const float* src = (s == R.rank) ? R.in : staged(R.peer[s], P.L);
+      const bool first = (k == 0);
+      for (uint64_t g = b + 4ull * lane; g < e; g += 4ull * 32 * 8) {
+        float4 v[8], a[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], v[k]);
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t i = g + 4ull * 32 * u;
+          if (i + 4 <= e) {
+            v[u] = __ldcg(reinterpret_cast<const float4*>(src + i));
+            a[u] = first ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldcg(reinterpret_cast<const float4*>(R.out + i));
+          } else if (i < e) {
+            float t[4] = {0, 0, 0, 0}, o[4] = {0, 0, 0, 0};
+            for (int q = 0; q < 4 && i + q < e; ++q) {
+              t[q] = __ldcg(src + i + q);
+              if (!first) o[q] = __ldcg(R.out + i + q);
+            }
+            v[u] = make_float4(t[0], t[1], t[2], t[3]);
+            a[u] = make_float4(o[0], o[1], o[2], o[3]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t i = g + 4ull * 32 * u;
+          if (i >= e) continue;
+          float4 r;
+          if (first && !P.zero_first) {
+            r = v[u];  // gather_to_root: acc = copy(local_root)
+          } else {   // fl(acc + x): with zero_first the first term is fl(0 + x_0)
+            r = make_float4(__fadd_rn(a[u].x, v[u].x), __fadd_rn(a[u].y, v[u].y), __fadd_rn(a[u].z, v[u].z),
+                            __fadd_rn(a[u].w, v[u].w));
+          }
+          if (i + 4 <= e) {
+            *reinterpret_cast<float4*>(R.out + i) = r;
+          } else {
+            const float t[4] = {r.x, r.y, r.z, r.w};
+            for (int q = 0; q < 4 && i + q < e; ++q) R.out[i + q] = t[q];
+          }
+        }
       }
-      if (m == 4) {
-        *reinterpret_cast<float4*>(R.out + g) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      } else {
-        for (int k = 0; k < m; ++k) R.out[g + k] = acc[k];
-      }
+      __syncwarp();  // this lane's next pass reads back what it wrote (same addresses)
     }
   }
 }

@@ -1,7 +1,8 @@
 #!/bin/bash
 # BASELINE.json configs on 1/2/4 GPUs of one box: one bench.py JSON line each.
-#   C2 small CNN trunc16 width 2 (the bench line), C3 AlexNet quant8 width 2,
-#   C4 ResNet-50 width 2 vs synchronous width 1.
+#   C1 MLP (width 2, none), C2 small CNN trunc16 (the bench line) with the
+#   paper's three schemes, C3 AlexNet quant8 three schemes, C4 ResNet-50
+#   width 2 vs width 1.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/matrix
 NG=$(nvidia-smi -L | wc -l)
@@ -16,11 +17,15 @@ run() {  # name ngpu args...
   fi
   echo "$name exit $?"
 }
+Q="--no-cpu-baseline --no-allreduce-sweep"
 for n in 1 2 4; do
-  run c2_n$n $n --steps 50 --warmup 10 --no-cpu-baseline ${EXTRA}
-done
-for n in 1 2 4; do
-  run c3_q8_n$n $n --model c3 --codec quant8 --global-batch 256 --steps 10 --warmup 3 --no-cpu-baseline --no-allreduce-sweep
-  run c4_pipe_n$n $n --model c4 --codec none --global-batch 256 --steps 10 --warmup 3 --no-cpu-baseline --no-allreduce-sweep
-  run c4_sync_n$n $n --model c4 --codec none --mode d_sync --global-batch 256 --steps 10 --warmup 3 --no-cpu-baseline --no-allreduce-sweep
+  run c1_pipe_n$n $n --model c1 --codec none --global-batch 100 --steps 300 --warmup 30 $Q
+  run c2_pipe_n$n $n --steps 100 --warmup 10 $Q
+  run c2_sync_n$n $n --mode d_sync --steps 100 --warmup 10 $Q
+  run c2_ps_n$n $n --mode ps_sync --steps 100 --warmup 10 $Q
+  run c3_pipe_n$n $n --model c3 --codec quant8 --global-batch 256 --steps 20 --warmup 5 $Q
+  run c3_sync_n$n $n --model c3 --codec quant8 --mode d_sync --global-batch 256 --steps 20 --warmup 5 $Q
+  run c3_ps_n$n $n --model c3 --codec quant8 --mode ps_sync --global-batch 256 --steps 20 --warmup 5 $Q
+  run c4_pipe_n$n $n --model c4 --codec none --global-batch 256 --steps 10 --warmup 3 $Q
+  run c4_sync_n$n $n --model c4 --codec none --mode d_sync --global-batch 256 --steps 10 --warmup 3 $Q
 done
