@@ -242,6 +242,7 @@ def workload_config(args, n, N):
             "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
             "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
             "cuda_graphs": bool(args.graphs) and args.mode == "pipe_sgd" and bool(args.fused),
+            "model_math": "fp32 (TF32 disabled for cuDNN convolutions and cuBLAS matmuls)",
             "l2": "not flushed: each step streams the model's activations for the per-GPU batch plus the "
                   "gradient, weights and slots through HBM"}
 
@@ -354,8 +355,13 @@ def our_arm(args, ws, rank, local):
             for _ in range(max(2, eng.K)):
                 step(t)
                 t += 1
+        prof = bool(os.environ.get("BENCH_PROFILE_RANGE"))
+        if prof:  # ncu --profile-from-start off: capture the timed region only
+            torch.cuda.profiler.start()
         with ClockSampler(local) as clk:
             ms_total, events = timed_region(t, args.steps, e2e=False)
+        if prof:
+            torch.cuda.profiler.stop()
         t += args.steps
         for _ in range(2):
             step(t)

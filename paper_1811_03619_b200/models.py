@@ -147,6 +147,17 @@ def build_torch_model(name: str) -> tuple[nn.Module, tuple, int]:
     raise ConfigError(f"unknown model {name!r}")
 
 
+def full_fp32_math() -> None:
+    """Disable TF32 for cuDNN convolutions and cuBLAS matmuls.
+
+    torch enables TF32 convolutions by default (cudnn.allow_tf32=True), a
+    10-bit-mantissa product; the reference computes its models in float32 /
+    float64 (models.py:118-195), so the engine runs every model in full fp32."""
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.set_float32_matmul_precision("highest")
+
+
 class FlatModel:
     """A module whose parameters/gradients are views into flat CUDA buffers.
 
@@ -155,6 +166,7 @@ class FlatModel:
     is exactly the reference's flat layout)."""
 
     def __init__(self, module: nn.Module, device, init_flat: np.ndarray | None = None, grad_buffers: int = 1):
+        full_fp32_math()
         self.module = module.to(device)
         self.plist = [p for p in self.module.parameters() if p.requires_grad]
         self.num_params = sum(p.numel() for p in self.plist)
