@@ -55,7 +55,7 @@ def parse():
                     help="replay the steady-state pipelined step as CUDA graphs (pipe_sgd, fused)")
     ap.add_argument("--fused", type=int, default=1,
                     help="one comm kernel per step (pre-compress + ring + re-compress fused)")
-    ap.add_argument("--channels-last", type=int, default=1,
+    ap.add_argument("--channels-last", type=int, default=0,
                     help="feed NHWC activations to cuDNN (no NCHW<->NHWC transposes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-allreduce-sweep", action="store_true")
@@ -65,18 +65,52 @@ def parse():
 # ------------------------------------------------------------------ helpers
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    """SM clocks + throttle reasons sampled every few ms while the timed region
+    runs (NVML in a thread: nvidia-smi's own start-up is longer than a
+    150 ms timed region). Falls back to `nvidia-smi -lms 100`."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.005):
         self.device = device
+        self.period = period_s
         self.proc = None
+        self.nvml = None
         self.lines: list[str] = []
+        self.samples: list[tuple[float, float, set]] = []
+        self._stop = threading.Event()
+
+    def _nvml_sample(self):
+        m = self.nvml
+        sm = m.nvmlDeviceGetClockInfo(self.h, m.NVML_CLOCK_SM)
+        r = m.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        bits = [m.nvmlClocksEventReasonHwSlowdown, m.nvmlClocksEventReasonHwThermalSlowdown,
+                m.nvmlClocksEventReasonSwThermalSlowdown, m.nvmlClocksEventReasonSwPowerCap]
+        self.samples.append((float(sm), self.max_sm, {nm for nm, b in zip(self.NAMES, bits) if r & b}))
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001 - a failed sample is just skipped
+                pass
+            self._stop.wait(self.period)
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -92,6 +126,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nvml:
+            self._stop.set()
+            self._t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -101,7 +138,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s_mhz, m_mhz, rs in self.samples:
+            sm.append(s_mhz)
+            mx = max(mx, m_mhz)
+            reasons |= rs
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
@@ -111,13 +151,13 @@ class ClockSampler:
                 mx = max(mx, float(f[1]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[4:8]):
+            for nm, v in zip(self.NAMES, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def dist_info():
