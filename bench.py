@@ -52,7 +52,7 @@ def parse():
                     help="128-thread CTAs the ring kernel may occupy per GPU beside the compute stream")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
-                    help="replay the steady-state pipelined step as CUDA graphs (pipe_sgd, fused)")
+                    help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync, fused)")
     ap.add_argument("--fused", type=int, default=1,
                     help="one comm kernel per step (pre-compress + ring + re-compress fused)")
     ap.add_argument("--channels-last", type=int, default=0,
@@ -281,7 +281,7 @@ def workload_config(args, n, N):
             "model": model, "params": n, "global_batch": args.global_batch,
             "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
             "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
-            "cuda_graphs": bool(args.graphs) and args.mode == "pipe_sgd" and bool(args.fused),
+            "cuda_graphs": bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused),
             "model_math": "fp32 (TF32 disabled for cuDNN convolutions and cuBLAS matmuls)",
             "l2": "not flushed: each step streams the model's activations for the per-GPU batch plus the "
                   "gradient, weights and slots through HBM"}
@@ -325,7 +325,7 @@ def our_arm(args, ws, rank, local):
     x_buf = torch.empty_like(x_dev)  # keeps x_dev's memory format
     y_buf = torch.empty_like(y_dev)
 
-    use_graphs = bool(args.graphs) and args.mode == "pipe_sgd" and bool(args.fused)
+    use_graphs = bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused)
 
     def batch_fn(r, t):
         if mode["e2e"]:  # host->device copy of this step's batch from pinned memory

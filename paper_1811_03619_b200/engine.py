@@ -390,7 +390,14 @@ class RankEngine:
 
     # --------------------------------------------------------- CUDA graphs
     def capture_graphs(self, batch) -> None:
-        """Capture the steady-state pipelined iteration as 2K CUDA graphs.
+        """Capture the steady-state iteration as CUDA graphs.
+
+        d_sync: K graphs on the compute stream, parity i = t % K: consume the
+        sum of t-1 + forward/backward into gradient buffer i + the fused ring
+        into the fp32 sum (nothing to overlap, so one stream; same kernels and
+        order as step_sync).
+
+        pipe_sgd: 2K graphs.
 
         For parity i = t % K: compute graph i (compute stream) = consume slot i
         + forward/backward of `batch` into gradient buffer i; comm graph i
@@ -401,8 +408,9 @@ class RankEngine:
         Requirements: pipe mode, fused path, real GPU transport, constant
         learning rate, static batch tensors (refilled in place by the caller)."""
         cfg = self.cfg
-        if not self.fused or cfg.mode != MODE_PIPE_SGD or cfg.lr_decay_every > 0 or self.grad_fn is not None:
-            raise ConfigError("graph mode needs fused pipe_sgd with a constant learning rate and a model")
+        if (not self.fused or cfg.mode not in (MODE_PIPE_SGD, MODE_D_SYNC) or cfg.lr_decay_every > 0
+                or self.grad_fn is not None):
+            raise ConfigError("graph mode needs fused pipe_sgd or d_sync with a constant learning rate and a model")
         if type(self.ep).__name__ == "EmulatedEndpoint":
             raise ConfigError("graph mode needs one GPU per rank (the emulated ring rendezvouses on the host)")
         x, y = batch
@@ -411,6 +419,9 @@ class RankEngine:
         self.g_compute, self.g_comm = [], []
         self.ev_agg = [torch.cuda.Event() for _ in range(self.K)]
         torch.cuda.synchronize(self.dev)
+        if cfg.mode == MODE_D_SYNC:
+            self._capture_sync_graphs(x, y, lr)
+            return
         for i in range(self.K):
             slot = self.slots[i]
             gc = torch.cuda.CUDAGraph()
@@ -431,8 +442,48 @@ class RankEngine:
             self.g_comm.append(gm)
         self.graph_ready_tag = {}
 
+    def _capture_sync_graphs(self, x, y, lr) -> None:
+        K, codec = self.K, self.cfg.codec
+        for i in range(K):
+            pend = self.sync_slots[(i - 1) % K]  # holds the sum of t-1 when t % K == i
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
+                _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
+                          pend.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+                self.fm.use_grad_buffer(i)
+                self.static_loss[i].copy_(self.fm.loss_and_grad(x, y))
+                g = self.fm.grad_bufs[i]
+                if self.world > 1:
+                    allreduce_into(g, self.summed, self.ep, codec, 0, self.cs, precompress=True)
+                else:
+                    roundtrip_async(g, codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+            self.g_compute.append(gc)
+        self.graph_pending = None
+
+    def _step_graph_sync(self, t: int) -> None:
+        """d_sync by replay: the graph consumes t-1 itself, so only an eager
+        predecessor (the warm-up's last step) has to be waited for."""
+        i = t % self.K
+        if self.graph_pending is None:
+            if self._pending is None or self._pending != t - 1:
+                raise ConfigError("d_sync graph replay needs the eager step t-1 just before")
+            self.buffer.take(self._pending, self.cs)
+            self._pending = None
+        elif self.graph_pending != t - 1:
+            raise ConfigError("d_sync graph steps must be consecutive")
+        e0 = self._ev(self.cs) if self.tracing else None
+        self.g_compute[i].replay()
+        self.losses[t].copy_(self.static_loss[i])
+        if self.tracing:
+            self._rec(t, STAGE_BACKWARD, e0, self._ev(self.cs))
+        self.graph_pending = t
+        self._mark(t)
+
     def step_graph(self, t: int) -> None:
-        """One pipelined iteration by graph replay (after prime / eager warm-up)."""
+        """One iteration by graph replay (after prime / eager warm-up)."""
+        if self.cfg.mode == MODE_D_SYNC:
+            self._step_graph_sync(t)
+            return
         i = t % self.K
         prev = self.graph_ready_tag.pop(i, None)
         if prev is not None:
@@ -458,6 +509,13 @@ class RankEngine:
 
     def drain_graph(self, t1: int) -> None:
         lr = float(np.float32(self.cfg.learning_rate))
+        if self.cfg.mode == MODE_D_SYNC:
+            if self.graph_pending is not None:
+                pend = self.sync_slots[self.graph_pending % self.K]
+                _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
+                          pend.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+                self.graph_pending = None
+            return
         for tag in range(t1 - self.K + 1, t1 + 1):
             i = tag % self.K
             self.cs.wait_event(self.ev_agg[i])

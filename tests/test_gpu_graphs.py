@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def train(P, p, codec, graphs, T=12, W=3):
+def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd"):
     from paper_1811_03619_b200.engine import RankEngine, RunConfig
     from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
     spec = ModelSpec("mlp", (64, 128, 10))
@@ -26,12 +26,15 @@ def train(P, p, codec, graphs, T=12, W=3):
             g = torch.Generator(device="cpu").manual_seed(10 + r)
             x = torch.randn(32, 64, generator=g).to(dev)
             y = torch.randint(0, 10, (32,), generator=g).to(dev)
-            cfg = RunConfig(mode="pipe_sgd", iterations=T + 2, learning_rate=0.05, codec=codec, batch_size=32)
+            cfg = RunConfig(mode=mode, iterations=T + 2, learning_rate=0.05, codec=codec, batch_size=32)
             eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False)
+            pipe = mode == "pipe_sgd"
+            step = eng.step if pipe else eng.step_sync
             with torch.cuda.stream(eng.cs):
-                eng.prime(1)
+                if pipe:
+                    eng.prime(1)
                 for t in range(1, W + 1):
-                    eng.step(t)
+                    step(t)
                 if graphs:
                     eng.capture_graphs((x, y))
                     for t in range(W + 1, T + 1):
@@ -39,8 +42,8 @@ def train(P, p, codec, graphs, T=12, W=3):
                     eng.drain_graph(T)
                 else:
                     for t in range(W + 1, T + 1):
-                        eng.step(t)
-                    eng.drain(T)
+                        step(t)
+                    eng.drain(T) if pipe else eng.drain_sync()
             torch.cuda.synchronize(dev)
             ep._check_errors(fm.num_params)
             return fm.params.cpu().numpy(), eng.losses[1:T + 1].cpu().numpy()
@@ -51,13 +54,14 @@ def train(P, p, codec, graphs, T=12, W=3):
         tr.close()
 
 
+@pytest.mark.parametrize("mode", ["pipe_sgd", "d_sync"])
 @pytest.mark.parametrize("codec", [0, 1, 2])
 @pytest.mark.parametrize("p", [1, 2])
-def test_graph_replay_matches_eager(P, p, codec):
+def test_graph_replay_matches_eager(P, p, codec, mode):
     if p > NGPU:
         pytest.skip("needs more GPUs")
-    eager = train(P, p, codec, graphs=False)
-    graph = train(P, p, codec, graphs=True)
+    eager = train(P, p, codec, graphs=False, mode=mode)
+    graph = train(P, p, codec, graphs=True, mode=mode)
     for r in range(p):
         assert_bits_equal(graph[r][0], eager[r][0], f"p={p} codec={codec} rank {r} weights")
         np.testing.assert_array_equal(graph[r][1], eager[r][1])

@@ -7,14 +7,16 @@ import sys
 ROWS = [("c1_pipe", "C1 MNIST MLP, none", "Pipe-SGD width 2 (graphs)"),
         ("c2_pipe", "C2 CIFAR CNN, trunc16", "Pipe-SGD width 2 (graphs)"),
         ("c2_pipe_eager", "C2 CIFAR CNN, trunc16", "Pipe-SGD width 2 (eager)"),
-        ("c2_sync", "C2 CIFAR CNN, trunc16", "D-Sync width 1 (eager)"),
+        ("c2_sync", "C2 CIFAR CNN, trunc16", "D-Sync width 1 (graphs)"),
+        ("c2_sync_eager", "C2 CIFAR CNN, trunc16", "D-Sync width 1 (eager)"),
         ("c2_ps", "C2 CIFAR CNN, trunc16", "PS-Sync (eager)"),
         ("c3_pipe", "C3 AlexNet, quant8", "Pipe-SGD width 2 (graphs)"),
         ("c3_pipe_eager", "C3 AlexNet, quant8", "Pipe-SGD width 2 (eager)"),
-        ("c3_sync", "C3 AlexNet, quant8", "D-Sync width 1 (eager)"),
+        ("c3_sync", "C3 AlexNet, quant8", "D-Sync width 1 (graphs)"),
+        ("c3_sync_eager", "C3 AlexNet, quant8", "D-Sync width 1 (eager)"),
         ("c3_ps", "C3 AlexNet, quant8", "PS-Sync (eager)"),
         ("c4_pipe", "C4 ResNet-50, none", "Pipe-SGD width 2 (graphs)"),
-        ("c4_sync", "C4 ResNet-50, none", "D-Sync width 1 (eager)")]
+        ("c4_sync", "C4 ResNet-50, none", "D-Sync width 1 (graphs)")]
 
 
 def load(d, name):
@@ -41,7 +43,7 @@ def main(d):
     print()
     print("Speed-ups at N=4:")
     for m in ("c2", "c3", "c4"):
-        for a, b in (("pipe", "sync"), ("pipe_eager", "sync"), ("pipe", "ps"), ("pipe_eager", "ps")):
+        for a, b in (("pipe", "sync"), ("pipe_eager", "sync_eager"), ("pipe", "ps"), ("pipe_eager", "ps")):
             x, y = vals.get((f"{m}_{a}", 4)), vals.get((f"{m}_{b}", 4))
             if x and y:
                 print(f"- {m.upper()}: {a} / {b} = {x / y:.2f}x")

@@ -23,9 +23,11 @@ for n in 1 2 4; do
   run c2_pipe_n$n $n --steps 100 --warmup 10 $Q
   run c2_pipe_eager_n$n $n --graphs 0 --steps 100 --warmup 10 $Q
   run c2_sync_n$n $n --mode d_sync --steps 100 --warmup 10 $Q
+  run c2_sync_eager_n$n $n --mode d_sync --graphs 0 --steps 100 --warmup 10 $Q
   run c2_ps_n$n $n --mode ps_sync --steps 100 --warmup 10 $Q
   run c3_pipe_n$n $n --model c3 --codec quant8 --global-batch 256 --steps 20 --warmup 5 $Q
   run c3_sync_n$n $n --model c3 --codec quant8 --mode d_sync --global-batch 256 --steps 20 --warmup 5 $Q
+  run c3_sync_eager_n$n $n --model c3 --codec quant8 --mode d_sync --graphs 0 --global-batch 256 --steps 20 --warmup 5 $Q
   run c3_ps_n$n $n --model c3 --codec quant8 --mode ps_sync --global-batch 256 --steps 20 --warmup 5 $Q
   run c4_pipe_n$n $n --model c4 --codec none --global-batch 256 --steps 10 --warmup 3 $Q
   run c3_pipe_eager_n$n $n --model c3 --codec quant8 --graphs 0 --global-batch 256 --steps 20 --warmup 5 $Q
