@@ -23,7 +23,17 @@ void gp_set_error_string(const std::string& m);  // comm.cu: the thread's last e
 namespace {
 
 constexpr int kT = 256;
-constexpr int kU = 4;  // groups per thread per streaming iteration
+#ifndef PIPESGD_CU_ELEMS
+#define PIPESGD_CU_ELEMS 16
+#endif
+#ifndef PIPESGD_CU_MINB
+#define PIPESGD_CU_MINB 1
+#endif
+// fp32 elements per thread per streaming iteration, the same for every
+// codec: kU<E> = 16 / E groups of E elements (4 x fp32 groups, 2 x trunc16,
+// 1 x quant8), so registers and bytes in flight do not grow with E.
+constexpr int kElems = PIPESGD_CU_ELEMS;
+template <int E> constexpr int kU = kElems / E > 0 ? kElems / E : 1;
 
 int cfail(int code, const std::string& m);
 
@@ -35,8 +45,8 @@ uint32_t grid_for(uint64_t n) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const uint64_t groups = (n + 3) / 4;
-  const uint64_t want = (groups + kT * kU - 1) / (kT * kU);
+  const uint64_t per_block = (uint64_t)kT * std::max(kElems, 16);
+  const uint64_t want = (n + per_block - 1) / per_block;
   const uint64_t cap = (uint64_t)sms * 8;
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
@@ -50,15 +60,16 @@ uint32_t grid_for(uint64_t n) {
 // thread for these short HBM-bound kernels).
 template <int E, typename L, typename S>
 __device__ __forceinline__ void stream_groups(uint64_t n, L&& load, S&& use) {
+  constexpr int U = kU<E>;
   const uint64_t stride = (uint64_t)E * kT * gridDim.x;
-  for (uint64_t base = (uint64_t)E * (blockIdx.x * (uint64_t)kT + threadIdx.x); base < n; base += stride * kU) {
+  for (uint64_t base = (uint64_t)E * (blockIdx.x * (uint64_t)kT + threadIdx.x); base < n; base += stride * U) {
     using T = decltype(load(base));
-    T v[kU];
+    T v[U];
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
+    for (int u = 0; u < U; ++u)
       if (base + u * stride < n) v[u] = load(base + u * stride);
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
+    for (int u = 0; u < U; ++u)
       if (base + u * stride < n) use(base + u * stride, v[u]);
   }
 }
@@ -91,7 +102,7 @@ __device__ __forceinline__ Q8 status_scale(gp_codec_status* st) {
 }
 
 template <int C>
-__global__ void __launch_bounds__(kT) encode_kernel(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(kT, PIPESGD_CU_MINB) encode_kernel(const float* __restrict__ x, uint64_t n,
                                                     uint8_t* payload, gp_codec_status* st) {
   constexpr int E = CodecT<C>::E;
   const Q8 q = status_scale<C>(st);
@@ -126,7 +137,7 @@ __global__ void __launch_bounds__(kT) roundtrip_kernel(const float* __restrict__
 }
 
 template <int C>
-__global__ void __launch_bounds__(kT) consume_update_kernel(float* w, const uint8_t* slot, const float* scale,
+__global__ void __launch_bounds__(kT, PIPESGD_CU_MINB) consume_update_kernel(float* w, const uint8_t* slot, const float* scale,
                                                             uint64_t n, float lr, int p) {
   constexpr int E = CodecT<C>::E;
   const float s = (C == kQuant8) ? *scale : 0.f;

@@ -39,17 +39,23 @@ def series(fn, with_flush):
     return e0.elapsed_time(e1) / R * 1e3
 
 
-kern = {
-    "torch_copy_37.7MB": lambda: loc.copy_(g),
-    "roundtrip_trunc16_37.7MB": lambda: roundtrip_async(g, 1, loc, st, s.cuda_stream),
-    "encode_trunc16_28.3MB": lambda: encode_async(g, 1, payload, st, s.cuda_stream),
-    "consume_update_trunc16_47.1MB": lambda: _lib.call("gp_consume_update", w.data_ptr(), 1, payload.data_ptr(),
-                                                       st.scale_view.data_ptr(), n, 1e-3, 1, s.cuda_stream),
-}
+payload4 = torch.zeros(n * 4, dtype=torch.uint8, device=dev)
+sts = [CodecStatus(dev) for _ in range(3)]
+for c in range(3):
+    encode_async(g, c, payload4, sts[c], s.cuda_stream)
+W = {0: 4, 1: 2, 2: 1}
+kern = {"torch_copy_37.7MB": lambda: loc.copy_(g)}
+for c, nm in ((0, "none"), (1, "trunc16"), (2, "quant8")):
+    kern[f"encode_{nm}_{(4 + W[c]) * n / 1e6:.1f}MB"] = (
+        lambda c=c: encode_async(g, c, payload4, sts[c], s.cuda_stream))
+    kern[f"consume_update_{nm}_{(8 + W[c]) * n / 1e6:.1f}MB"] = (
+        lambda c=c: _lib.call("gp_consume_update", w.data_ptr(), c, payload4.data_ptr(),
+                              sts[c].scale_view.data_ptr(), n, 1e-3, 2, s.cuda_stream))
+kern["roundtrip_trunc16_37.7MB"] = lambda: roundtrip_async(g, 1, loc, st, s.cuda_stream)
 base = series(None, True)
 series(None, True)
 for k, fn in kern.items():
     fn()
     warm = series(fn, False)
     cold = series(fn, True) - series(None, True)
-    print(json.dumps({"kernel": k, "n": n, "warm_us": round(warm, 2), "cold_us": round(cold, 2)}), flush=True)
+    print(json.dumps({"lib": os.path.basename(os.environ.get("PIPESGD_LIB", "default")), "kernel": k, "n": n, "warm_us": round(warm, 2), "cold_us": round(cold, 2)}), flush=True)
