@@ -465,8 +465,9 @@ def our_arm(args, ws, rank, local):
                 "bound": "nvlink", "achieved": kr["isolated_nvlink_gbs"], "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": kr["isolated_nvlink_gbs"] / NVLINK_PEAK_GBS,
                 "traffic": None,
-                "measured": "kernel alone on the step's gradient (L2 flushed, ranks barrier-aligned, median of "
-                            "launches); in the pipeline the same launch also waits for slower ranks: "
+                "measured": "kernel alone on the step's gradient, 20 back-to-back launches each after a 256 MiB "
+                            "L2-evicting read, minus the same series without the kernel; in the pipeline "
+                            "(sharing the SMs with the CNN, waiting for slower ranks): "
                             f"{kr['in_pipeline_nvlink_gbs'] or 0:.1f} GB/s",
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (MEASURED_PEAKS.json has "
                                "no NVLink entry); this pool's bidirectional push ceiling measured by "
@@ -560,28 +561,21 @@ def isolated_kernels(eng, codec, N, dev, reps=20):
     lr = float(np.float32(1e-3))
 
     def timeit(fn, sync_ranks=False):
-        if sync_ranks:  # cross-GPU kernel: align ranks before each launch, median
-            ts = []
-            for r in range(reps + 1):
-                with torch.cuda.stream(s):
-                    flush.sum()
-                s.synchronize()
-                dist.barrier()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-                fn()
-                e1.record(s)
-                e1.synchronize()
-                if r:
-                    ts.append(e0.elapsed_time(e1))
-            return float(np.median(ts))
-        # single-GPU kernel: R x (flush) and R x (flush + kernel) back to back,
-        # so the stream never idles between launches; the difference is the
-        # kernel's own cold-L2 time without launch gaps.
+        # R x (flush) and R x (flush + kernel) back to back, so the stream
+        # never idles between launches; the difference / R is the kernel's
+        # own cold-L2 time without launch gaps. A ~2 ms GPU sleep ahead of
+        # the first event lets the host enqueue the whole series before the
+        # clock starts (a Python-side launch is slower than these kernels).
+        # Cross-GPU kernels: one barrier before each series; the ring's flag
+        # waits keep the ranks in lockstep from there on.
         def series(with_kernel):
+            s.synchronize()
+            if sync_ranks:
+                dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(s):
                 flush.sum()
+                torch.cuda._sleep(4_000_000)
                 e0.record(s)
                 for _ in range(reps):
                     flush.sum()

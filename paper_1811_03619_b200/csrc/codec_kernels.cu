@@ -24,14 +24,17 @@ namespace {
 
 constexpr int kT = 256;
 #ifndef PIPESGD_CU_ELEMS
-#define PIPESGD_CU_ELEMS 16
+#define PIPESGD_CU_ELEMS 8
 #endif
 #ifndef PIPESGD_CU_MINB
 #define PIPESGD_CU_MINB 1
 #endif
 // fp32 elements per thread per streaming iteration, the same for every
-// codec: kU<E> = 16 / E groups of E elements (4 x fp32 groups, 2 x trunc16,
-// 1 x quant8), so registers and bytes in flight do not grow with E.
+// codec: kU<E> = max(1, 8 / E) groups of E elements (2 x fp32 groups, 1 x
+// trunc16, 1 x quant8), so registers do not grow with E. Measured cold-L2
+// at 4.7 M elements against 16/32 elements and the earlier 4-groups-of-any-E
+// loop (profiles/r01_final/codec_kernel_variants.md): consume_update
+// trunc16 19.4 -> 16.7 us, quant8 33.9 -> 19.1 us.
 constexpr int kElems = PIPESGD_CU_ELEMS;
 template <int E> constexpr int kU = kElems / E > 0 ? kElems / E : 1;
 

@@ -254,6 +254,12 @@ __device__ __forceinline__ void stamp(const RingParams& P, uint32_t wid, int lra
     P.trace[((uint64_t)lrank * P.G * kWarps + wid) * kTraceSlots + k] = globaltimer();
 }
 
+// p == 2 only (slots 4..13 belong to reduce-scatter steps s >= 1 otherwise):
+// finer per-chunk stamps for the fold phase, first chunk of each warp.
+__device__ __forceinline__ void stamp2(const RingParams& P, uint32_t wid, int lrank, int k, bool on) {
+  if (on && P.p == 2) stamp(P, wid, lrank, k);
+}
+
 // Dynamic chunk scheduling: the warps of one rank take chunk indices of a
 // phase from a counter in the rank's control block (reset when the call
 // closes). Flags are per chunk, not per warp, so ranks need not agree on
@@ -369,13 +375,17 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       stamp(P, wid, lr, 16);
     }
     uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
+    bool first0 = true;
     for (uint32_t c = grab(ctl, 1); c < B.nch; c = grab(ctl, 1)) {
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
                       store_pay<C>(dst, g0 - B.A, vlo, vhi, encode_v<C>(px(v), q, bad));
                     });
+      stamp2(P, wid, lr, 7, first0);
       warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
+      stamp2(P, wid, lr, 8, first0);
+      first0 = false;
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhRS, 0, r, r, 0);
     bad = 0;
@@ -420,16 +430,19 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       bool first = true;
       for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
         float sin;
+        stamp2(P, wid, lr, 4, first);
         if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
         if (first) stamp(P, wid, lr, 2 + 2 * s);
-        first = false;
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                         emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
                              0.f);
                       });
+        stamp2(P, wid, lr, 5, first);
         if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
         else publish_last(c, 0.f);
+        stamp2(P, wid, lr, 6, first);
+        first = false;
       }
     } else {
       // pass A: fold into `out` (scratch for this block) and reduce the max
@@ -510,6 +523,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     bool first = true;
     for (uint32_t c = grab(ctl, 20 + k); c < B.nch; c = grab(ctl, 20 + k)) {
       float sin;
+      stamp2(P, wid, lr, 9, first && k == 1);
       if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) return;
       if (k == 1 && first) stamp(P, wid, lr, 18);
       first = false;

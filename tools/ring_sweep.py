@@ -32,6 +32,8 @@ def timed(fn, iters, warmup, stream):
     stream.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(2_000_000)  # host enqueues the whole series before the clock starts
     a.record(stream)
     for _ in range(iters):
         fn()

@@ -25,6 +25,7 @@ ap.add_argument("--numel", type=int, default=1 << 22)
 ap.add_argument("--codec", default="trunc16")
 ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--fused", type=int, default=0, help="engine form: precompress + compressed slot output")
 a = ap.parse_args()
 local = int(os.environ.get("LOCAL_RANK", 0))
 torch.cuda.set_device(local)
@@ -37,9 +38,12 @@ tr = torch.zeros(W * 20, dtype=torch.int64, device="cuda")
 x = torch.randn(a.numel, device="cuda")
 y = torch.empty_like(x)
 codec = Codec.parse(a.codec)
+slot = torch.empty(a.numel * codec.bytes_per_elem, dtype=torch.uint8, device="cuda")
+slot_scale = torch.empty(1, device="cuda")
+kw = dict(precompress=True, slot=slot, slot_scale=slot_scale) if a.fused else {}
 s = torch.cuda.current_stream()
 for _ in range(3):
-    allreduce_into(x, y, ep, codec, 0, s)
+    allreduce_into(x, y, ep, codec, 0, s, **kw)
 endpoint_wait(ep, a.numel, s)
 res = []
 for rep in range(a.reps):
@@ -48,7 +52,7 @@ for rep in range(a.reps):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    allreduce_into(x, y, ep, codec, 0, s)
+    allreduce_into(x, y, ep, codec, 0, s, **kw)
     e1.record(s)
     endpoint_wait(ep, a.numel, s)
     _lib.call("gp_comm_set_trace", ep._comm, None)
@@ -58,7 +62,9 @@ for rep in range(a.reps):
              16: "q8_bar0_out", 17: "q8_s0_bar_out"}
     if p == 2:
         names[15] = "q8_s0_passA_done"
-    for s_ in range(1, p - 1):
+        names.update({4: "fold_first_grab", 5: "fold_first_data_done", 6: "fold_first_published",
+                      7: "send_first_data_done", 8: "send_first_published", 9: "ag_first_grab"})
+    for s_ in range(1, p - 1) if p > 2 else ():
         names[2 + 2 * s_] = f"s{s_}_first_in"
         names[3 + 2 * s_] = f"s{s_}_done"
     row = {"event_us": e0.elapsed_time(e1) * 1e3, "kernel_span_us": (t[:, 19].max() - t0) / 1e3,
@@ -71,6 +77,6 @@ for rep in range(a.reps):
             row[nm] = [round(float(z), 1) for z in q]
     res.append(row)
 if rank == 0:
-    print(json.dumps({"n": a.numel, "codec": a.codec, "p": p, "ctas": G, "reps": res[-2:]}, indent=1))
+    print(json.dumps({"n": a.numel, "codec": a.codec, "p": p, "ctas": G, "fused": a.fused, "reps": res[-2:]}, indent=1))
 dist.barrier()
 dist.destroy_process_group()
