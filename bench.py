@@ -461,31 +461,37 @@ def our_arm(args, ws, rank, local):
         kr["wire_bytes"] = wire
         kr["isolated_nvlink_gbs"] = wire / (iso["ring"] * 1e-3) / 1e9
         kr["in_pipeline_nvlink_gbs"] = wire / (avg["ring"] * 1e-3) / 1e9 if avg.get("ring") else None
+        live = kr["in_pipeline_nvlink_gbs"] or kr["isolated_nvlink_gbs"]
         roof = {"kernel": "ring_allreduce_kernel<%s> (fused decode+add+encode+NVLink push)" % args.codec,
-                "bound": "nvlink", "achieved": kr["isolated_nvlink_gbs"], "peak": NVLINK_PEAK_GBS,
-                "unit": "GB/s", "frac": kr["isolated_nvlink_gbs"] / NVLINK_PEAK_GBS,
+                "bound": "nvlink", "achieved": live, "peak": NVLINK_PEAK_GBS,
+                "unit": "GB/s", "frac": live / NVLINK_PEAK_GBS,
                 "traffic": None,
-                "measured": "kernel alone on the step's gradient, 20 back-to-back launches each after a 256 MiB "
-                            "L2-evicting read, minus the same series without the kernel; in the pipeline "
-                            "(sharing the SMs with the CNN, waiting for slower ranks): "
-                            f"{kr['in_pipeline_nvlink_gbs'] or 0:.1f} GB/s",
+                "traffic_note": "ncu cannot profile the multi-process ring; the emulated capture in "
+                                "profiles/r01_final/ncu_summary.md has its HBM traffic",
+                "measured": "CUDA events on the comm stream around every ring launch of the timed region "
+                            "(the launch shares the SMs with the CNN and waits for the slower rank); the same "
+                            "kernel alone (20 back-to-back launches after L2-evicting reads, minus the reads): "
+                            f"{kr['isolated_nvlink_gbs']:.1f} GB/s",
+                "achieved_isolated": kr["isolated_nvlink_gbs"],
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (MEASURED_PEAKS.json has "
                                "no NVLink entry); this pool's bidirectional push ceiling measured by "
                                "gp_calib_p2p_copy is ~690-707 GB/s",
                 "algorithmic_bytes_per_launch": wire}
     else:
         copy_gbs = 8 * n / (iso["copy_4n"] * 1e-3) / 1e9
-        dom = max([k for k in ("update", "compress", "recompress") if k in kernels and iso.get(k)],
-                  key=lambda k: avg.get(k, 0.0))
+        dom = max([k for k in ("update", "compress", "recompress") if k in kernels and avg.get(k)],
+                  key=lambda k: avg[k])
         name = {"update": "consume_update_kernel", "compress": "roundtrip_kernel",
                 "recompress": "encode_kernel"}[dom]
         kd = kernels[dom]
-        roof = {"kernel": name, "bound": "hbm", "achieved": kd["isolated_hbm_gbs"], "peak": hbm_peak,
-                "unit": "GB/s", "frac": kd["isolated_hbm_gbs"] / hbm_peak,
+        live = kd["in_pipeline_hbm_gbs"]
+        roof = {"kernel": name, "bound": "hbm", "achieved": live, "peak": hbm_peak,
+                "unit": "GB/s", "frac": live / hbm_peak,
                 "traffic": traffic.get(name),
-                "measured": "kernel alone on the step's buffers, L2 flushed before each launch; inside the "
-                            "pipeline it shares HBM with the other stream: "
-                            f"{kd.get('in_pipeline_hbm_gbs', 0):.1f} GB/s",
+                "measured": "CUDA events on the launching stream around every launch of the timed region "
+                            "(sharing HBM and SMs with the other stream); the same kernel alone, L2 flushed "
+                            f"before each launch: {kd.get('isolated_hbm_gbs', 0):.1f} GB/s",
+                "achieved_isolated": kd.get("isolated_hbm_gbs"),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
                 "same_size_torch_copy_gbs": copy_gbs,
                 "note": "at this vector size (%d fp32) launch/ramp latency bounds every kernel: torch's own "

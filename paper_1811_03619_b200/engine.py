@@ -397,11 +397,14 @@ class RankEngine:
         into the fp32 sum (nothing to overlap, so one stream; same kernels and
         order as step_sync).
 
-        pipe_sgd: 2K graphs.
+        pipe_sgd: for parity i = t % K: update graph i (compute stream) =
+        consume slot i; compute graph i = forward/backward of `batch` into
+        gradient buffer i; comm graph i (comm stream) = the fused ring from
+        gradient buffer i into slot i.
 
-        For parity i = t % K: compute graph i (compute stream) = consume slot i
-        + forward/backward of `batch` into gradient buffer i; comm graph i
-        (comm stream) = the fused ring from gradient buffer i into slot i.
+        Update, compute and comm are separate graphs (one extra graph launch
+        per step) so CUDA events between them time each of our kernels inside
+        the timed region.
         Replays are linked by events between the streams, so iteration t's
         ring still overlaps iteration t+1's compute. The ring kernel reads its
         call sequence number on the device, so every replay is a new call.
@@ -416,7 +419,7 @@ class RankEngine:
         x, y = batch
         lr = float(np.float32(cfg.learning_rate))
         self.static_loss = [torch.zeros((), dtype=torch.float32, device=self.dev) for _ in range(self.K)]
-        self.g_compute, self.g_comm = [], []
+        self.g_update, self.g_compute, self.g_comm = [], [], []
         self.ev_agg = [torch.cuda.Event() for _ in range(self.K)]
         torch.cuda.synchronize(self.dev)
         if cfg.mode == MODE_D_SYNC:
@@ -424,10 +427,13 @@ class RankEngine:
             return
         for i in range(self.K):
             slot = self.slots[i]
-            gc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
+            gu = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gu, stream=self.cs, capture_error_mode="thread_local"):
                 _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
                           slot.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+            self.g_update.append(gu)
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
                 self.fm.use_grad_buffer(i)
                 self.static_loss[i].copy_(self.fm.loss_and_grad(x, y))
             gm = torch.cuda.CUDAGraph()
@@ -446,18 +452,24 @@ class RankEngine:
         K, codec = self.K, self.cfg.codec
         for i in range(K):
             pend = self.sync_slots[(i - 1) % K]  # holds the sum of t-1 when t % K == i
-            gc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
+            gu = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gu, stream=self.cs, capture_error_mode="thread_local"):
                 _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
                           pend.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
                 self.fm.use_grad_buffer(i)
                 self.static_loss[i].copy_(self.fm.loss_and_grad(x, y))
+            gm = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gm, stream=self.cs, capture_error_mode="thread_local"):
                 g = self.fm.grad_bufs[i]
                 if self.world > 1:
                     allreduce_into(g, self.summed, self.ep, codec, 0, self.cs, precompress=True)
                 else:
                     roundtrip_async(g, codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+            self.g_update.append(gu)
             self.g_compute.append(gc)
+            self.g_comm.append(gm)
         self.graph_pending = None
 
     def _step_graph_sync(self, t: int) -> None:
@@ -471,11 +483,20 @@ class RankEngine:
             self._pending = None
         elif self.graph_pending != t - 1:
             raise ConfigError("d_sync graph steps must be consecutive")
-        e0 = self._ev(self.cs) if self.tracing else None
+        tr = self.tracing
+        e0 = self._ev(self.cs) if tr else None
+        self.g_update[i].replay()
+        e1 = self._ev(self.cs) if tr else None
         self.g_compute[i].replay()
         self.losses[t].copy_(self.static_loss[i])
-        if self.tracing:
-            self._rec(t, STAGE_BACKWARD, e0, self._ev(self.cs))
+        e2 = self._ev(self.cs) if tr else None
+        self.g_comm[i].replay()
+        if tr:
+            e3 = self._ev(self.cs)
+            self._rec(t, STAGE_UPDATE, e0, e1, t - 1)
+            self._rec(t, STAGE_BACKWARD, e1, e2)
+            self._rec(t, STAGE_ALLREDUCE, e2, e3)
+            self._rec(t, "ring" if self.world > 1 else "compress", e2, e3)
         self.graph_pending = t
         self._mark(t)
 
@@ -490,17 +511,21 @@ class RankEngine:
             self.cs.wait_event(self.ev_agg[i])
         else:  # slot i still holds the eager pipeline's tag t-K: wait for it
             self.buffer.take(t - self.K, self.cs)
-        e0 = self._ev(self.cs) if self.tracing else None
+        tr = self.tracing
+        e0 = self._ev(self.cs) if tr else None
+        self.g_update[i].replay()
+        eu = self._ev(self.cs) if tr else None
         self.g_compute[i].replay()
         self.losses[t].copy_(self.static_loss[i])
         self.ev_local[i].record(self.cs)
         self.ms.wait_event(self.ev_local[i])
-        e1 = self._ev(self.ms) if self.tracing else None
+        e1 = self._ev(self.ms) if tr else None
         with torch.cuda.stream(self.ms):
             self.g_comm[i].replay()
         self.ev_agg[i].record(self.ms)
-        if self.tracing:
-            self._rec(t, STAGE_BACKWARD, e0, self._ev(self.cs))
+        if tr:
+            self._rec(t, STAGE_UPDATE, e0, eu, t - self.K)
+            self._rec(t, STAGE_BACKWARD, eu, self._ev(self.cs))
             e2 = self._ev(self.ms)
             self._rec(t, STAGE_ALLREDUCE, e1, e2)
             self._rec(t, "ring" if self.world > 1 else "recompress", e1, e2)
