@@ -235,6 +235,23 @@ def cpu_path_rate(n, p, codec, seconds, max_iters=1000):
     return k / dt, k, dt
 
 
+def cpu_ring_times(n, codec, codec_name, ps=(2, 4)):
+    """The reference ring_allreduce (oracle port, collective.py:77-163) on
+    this host for the step's gradient: all p ranks simulated in one thread,
+    one call each (the SURVEY 8(d) CPU path beside the GPU ring)."""
+    from oracle.ring import ring_allreduce_all
+    g = np.random.default_rng(1)
+    out = []
+    for p in ps:
+        xs = [g.normal(0, 1e-2, n).astype(np.float32) for _ in range(p)]
+        t0 = time.perf_counter()
+        ring_allreduce_all(xs, codec)
+        dt = time.perf_counter() - t0
+        out.append({"p": p, "n": n, "codec": codec_name, "s_per_call_all_ranks": dt,
+                    "busbw_fp32_gbs": 2 * (p - 1) / p * 4 * n / dt / 1e9})
+    return out
+
+
 def reference_arm(args, ws, rank):
     if rank != 0:
         return None
@@ -727,7 +744,8 @@ def main():
             "value": v, "unit": "iters/s", "cores": 1, "kind": "port",
             "sample": (f"{k} iterations ({dt:.1f} s) of the oracle port of the reference hot path on the "
                        f"{line['config']['params']}-element gradient (codec, p=1 ring, re-compress, mean, SGD; "
-                       f"no CNN fwd/bwd: the reference has none); host {cpu_model()}")}
+                       f"no CNN fwd/bwd: the reference has none); host {cpu_model()}"),
+            "ring_allreduce": cpu_ring_times(line["config"]["params"], codec, args.codec)}
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()

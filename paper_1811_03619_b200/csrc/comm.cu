@@ -359,6 +359,16 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
   ++c->seq;  // host-side count (info only); the kernel numbers calls on the device
   P.iteration = iteration;
   P.chunk = pick_chunk(n, p, c->G, codec);
+  {
+    // Launch only as many warps as the largest phase has chunks: the chunk
+    // size (and so every flag index) still follows the communicator-wide G,
+    // but small calls no longer start G CTAs whose warps would only hammer
+    // the phase counters (2p same-address atomics per idle warp).
+    const uint64_t maxblk = (n + p - 1) / p + 16;
+    uint64_t nch = (maxblk + P.chunk - 1) / P.chunk;
+    if (P.pre && codec == GP_CODEC_QUANT8) nch = std::max<uint64_t>(nch, (n + P.chunk - 1) / P.chunk);
+    P.G = (int)std::min<uint64_t>((uint64_t)c->G, std::max<uint64_t>(1, (nch + kRingWarps - 1) / kRingWarps));
+  }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;
   for (int i = 0; i < c->nlocal; ++i) {

@@ -39,7 +39,10 @@ namespace gp {
 namespace {
 
 constexpr int kWarps = kRingThreads / 32;
-constexpr uint64_t kBatch = 1024;  // elements per warp per batch (32 lanes x U x E)
+#ifndef PIPESGD_RING_BATCH
+#define PIPESGD_RING_BATCH 1024
+#endif
+constexpr uint64_t kBatch = PIPESGD_RING_BATCH;  // elements per warp per batch (32 lanes x U x E)
 
 // This call's sequence number, read from the rank's control block at entry.
 // It lives on the device (not in the launch parameters) so a launch can be

@@ -1,5 +1,6 @@
 """Run the fused ring once per codec with p ranks emulated on cuda:0 (for ncu:
-`-k regex:ring_allreduce`). Checks bit-exactness against the oracle."""
+`-k regex:ring_allreduce`). Checks that every rank's output is bit-identical
+(parity against the oracle lives in tests/test_gpu_ring.py)."""
 import os
 import sys
 import threading
@@ -23,9 +24,7 @@ for codec in codecs:
           for r in range(p)]
     [t.start() for t in th]
     [t.join() for t in th]
-    if n <= (1 << 22):
-        from oracle import ring as OR
-        want = OR.ring_allreduce_all([x.cpu().numpy() for x in ins], int(codec)).outputs[0]
-        assert np.array_equal(outs[0].cpu().numpy().view(np.uint32), want.view(np.uint32))
+    for r in range(1, p):
+        assert torch.equal(outs[r].view(torch.int32), outs[0].view(torch.int32)), f"rank {r} differs"
     print(codec.name, "ok", flush=True)
 tr.close()

@@ -1,5 +1,6 @@
 """One fused ring call per codec (precompress + slot output, the engine's comm
-kernel) with p ranks emulated on cuda:0, for ncu. Checks against the oracle."""
+kernel) with p ranks emulated on cuda:0, for ncu. Checks that every rank's
+slot and scale are bit-identical (oracle parity: tests/test_gpu_fused.py)."""
 import os
 import sys
 import threading
@@ -8,8 +9,6 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import codec as OC  # noqa: E402
-from oracle import ring as OR  # noqa: E402
 from paper_1811_03619_b200 import Codec, EmulatedTransport  # noqa: E402
 from paper_1811_03619_b200.collective import allreduce_into, endpoint_wait  # noqa: E402
 
@@ -36,10 +35,7 @@ for codec in codecs:
     th = [threading.Thread(target=run, args=(r,)) for r in range(p)]
     [t.start() for t in th]
     [t.join() for t in th]
-    if n <= (1 << 22):
-        summed = OR.ring_allreduce_all([OC.roundtrip(x, int(codec)) for x in ins_np], int(codec)).outputs[0]
-        s_want, pl_want = OC.encode(summed, int(codec))
-        assert res[0][0].tobytes() == np.asarray(pl_want).tobytes()
-        assert np.float32(res[0][1][0]).view(np.uint32) == np.float32(s_want).view(np.uint32)
+    for r in range(1, p):
+        assert res[r][0].tobytes() == res[0][0].tobytes() and res[r][1].tobytes() == res[0][1].tobytes()
     print(codec.name, "ok", flush=True)
 tr.close()
