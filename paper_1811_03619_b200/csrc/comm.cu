@@ -52,7 +52,10 @@ Layout make_layout(int p, uint64_t max_elems) {
   L.off_hdr = 4096 + 256;
   L.off_flags = round_up(L.off_hdr + (uint64_t)L.nslot * sizeof(SlotHdr), 256);
   L.off_payload = round_up(L.off_flags + (uint64_t)L.nslot * L.max_chunks * 8, 4096);
-  L.total_bytes = L.off_payload + (uint64_t)L.nslot * L.slot_bytes;
+  L.ll_max_blk = std::min<uint64_t>(maxblk, kLLRegionBlock);
+  L.ll_slot_bytes = round_up(32 + 8 * (L.ll_max_blk + 32), 256);  // worst case fp32: 8 B per element
+  L.off_ll = L.off_payload + (uint64_t)L.nslot * L.slot_bytes;
+  L.total_bytes = L.off_ll + (uint64_t)L.nslot * L.ll_slot_bytes;
   return L;
 }
 
@@ -81,9 +84,12 @@ namespace {
 int alloc_inbox(gp_comm* c, int i) {
   cudaError_t e = cudaMalloc(&c->inbox[i], c->L.total_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(inbox)");
-  // Flags, headers, ctl and error word must start at zero; payload need not.
+  // Flags, headers, ctl, error word and the LL region (its words carry
+  // sequence numbers) must start at zero; payload need not.
   e = cudaMemset(c->inbox[i], 0, c->L.off_payload);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(inbox)");
+  e = cudaMemset(c->inbox[i] + c->L.off_ll, 0, c->L.total_bytes - c->L.off_ll);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(LL region)");
   e = cudaMemset(c->inbox[i] + c->L.off_err, 0xFF, sizeof(unsigned long long));  // no error
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(error word)");
   return GP_OK;
@@ -368,6 +374,7 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
     uint64_t nch = (maxblk + P.chunk - 1) / P.chunk;
     if (P.pre && codec == GP_CODEC_QUANT8) nch = std::max<uint64_t>(nch, (n + P.chunk - 1) / P.chunk);
     P.G = (int)std::min<uint64_t>((uint64_t)c->G, std::max<uint64_t>(1, (nch + kRingWarps - 1) / kRingWarps));
+    P.ll = (codec != GP_CODEC_QUANT8 && maxblk <= std::min<uint64_t>(kLLBlock, c->L.ll_max_blk)) ? 1 : 0;
   }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;
@@ -537,7 +544,7 @@ int gp_comm_poll_error(gp_comm* c, gp_error* out) {
   if (best != ~0ull) {
     static const int phases[4] = {kPhRS, kPhBarrier, kPhAG, kPhLocal};
     out->phase = phases[(best >> 60) & 0xF];
-    out->step = (int)((best >> 52) & 0xFF);
+    out->step = (int)((best >> 53) & 0x7F);  // bit 52: abort consequence (ordering only)
     out->kind = (int)((best >> 48) & 0xF);
     out->block = (int)((best >> 40) & 0xFF) - 1;
     out->rank = (int)((best >> 32) & 0xFF);

@@ -62,11 +62,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// Record a failure; the earliest (phase, step) is kept.
+// Record a failure; the earliest (phase, step) is kept, and at the same
+// (phase, step) a cause (header mismatch, own timeout, non-finite) beats a
+// wait that only ended because a peer aborted (timeout kind, detail 1): bit
+// 52 marks those consequences. Steps fit 7 bits (p <= 8).
 __device__ __forceinline__ void latch_error(ErrWord* e, int kind, int phase, int step, int block,
                                             int rank, int detail) {
+  const unsigned long long consequence = (kind == kErrTimeout && detail == 1) ? 1ull : 0ull;
   const unsigned long long code =
-      ((unsigned long long)(phase_order(phase) & 0xF) << 60) | ((unsigned long long)(step & 0xFF) << 52) |
+      ((unsigned long long)(phase_order(phase) & 0xF) << 60) | ((unsigned long long)(step & 0x7F) << 53) |
+      (consequence << 52) |
       ((unsigned long long)(kind & 0xF) << 48) | ((unsigned long long)((block + 1) & 0xFF) << 40) |
       ((unsigned long long)(rank & 0xFF) << 32) | (unsigned long long)(uint32_t)detail;
   atomicMin(&e->code, code);

@@ -8,18 +8,21 @@
 // so block b is the left fold s_0 = x_b, s_k = fl(x_{b+k} + D(C(s_{k-1})))
 // starting at rank b, and out[b] = D(C(s_{p-1})) on every rank.
 //
-// B200 mapping. One cooperative launch per rank per call: G CTAs x 16 warps.
-// Every WARP is an independent worker. A ring block is cut into chunks of
-// `chunk` elements (multiple of 1024, origin = block start rounded down to
-// 16); chunk c of every block belongs to warp c % (16G) on every rank, so
-// each chunk flows around the ring on its own:
+// B200 mapping. One launch per rank per call (cooperative when all ranks
+// are emulated on one GPU): up to G CTAs of 128 threads, every WARP an
+// independent worker. A ring block is cut into chunks of `chunk` elements
+// (multiple of 1024, origin = block start rounded down to 16); warps take
+// chunk indices of each phase from a per-rank counter, and every chunk flows
+// around the ring on its own:
 //   lane 0 acquires flag(slot s, chunk c) -> the warp streams the chunk in
 //   1024-element batches (each lane one 16-byte payload vector per group:
 //   4 fp32 / 8 trunc16 / 16 quant8 elements) -> decode inbox + add local ->
 //   encode -> st.global into succ's inbox over NVLink -> __syncwarp ->
-//   lane 0: fence.acq_rel.sys + st.release.sys succ's flag.
+//   lane 0: st.release.sys succ's flag.
+// Small none/trunc16 blocks use the LL protocol instead (sequence number in
+// every 8-byte word, no fence, no flag; see ll_put / ll_get).
 // No CTA-wide barrier sits on the data path, so a warp waiting on its fence
-// or flag never stalls the other 15 warps of its SM.
+// or flag never stalls the other warps of its SM.
 // quant8 needs the block-wide max before any code can be emitted
 // (compression.py:129-132): each of its hops is pass A (fold, park the
 // partial sum in `out`, reduce the max), a rank-wide barrier carrying the
@@ -72,6 +75,51 @@ __device__ __forceinline__ SlotHdr* hdr_ptr(uint8_t* inbox, const Layout& L, int
 }
 __device__ __forceinline__ uint8_t* slot_ptr(uint8_t* inbox, const Layout& L, int slot) {
   return inbox + L.off_payload + (uint64_t)slot * L.slot_bytes;
+}
+
+// ---- LL protocol (small blocks, ring.cuh:kLLBlock). A slot is a 32-byte
+// header line then one 32-byte line per 16-byte payload group; every 8-byte
+// word is {4 payload bytes, call sequence}, written with one 16-byte volatile
+// store per half line. Aligned 8-byte accesses are single-copy atomic, so a
+// word whose sequence half matches carries this call's payload half: the
+// receiver polls the data itself, no fence and no flag store.
+__device__ __forceinline__ uint8_t* ll_ptr(uint8_t* inbox, const Layout& L, int slot) {
+  return inbox + L.off_ll + (uint64_t)slot * L.ll_slot_bytes;
+}
+__device__ __forceinline__ void st_vol_v4(uint4* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_vol_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void ll_put(uint8_t* line, uint4 v) {
+  uint4* q = reinterpret_cast<uint4*>(line);
+  st_vol_v4(q, make_uint4(v.x, s_seq, v.y, s_seq));
+  st_vol_v4(q + 1, make_uint4(v.z, s_seq, v.w, s_seq));
+}
+// Poll one line; false if `give_up` turned true (timeout / abort seen).
+template <typename G>
+__device__ __forceinline__ bool ll_get(const uint8_t* line, uint4& out, G&& give_up) {
+  const uint4* q = reinterpret_cast<const uint4*>(line);
+  for (uint32_t it = 1;; ++it) {
+    const uint4 a = ld_vol_v4(q), b = ld_vol_v4(q + 1);
+    if (a.y == s_seq && a.w == s_seq && b.y == s_seq && b.w == s_seq) {
+      out = make_uint4(a.x, a.z, b.x, b.z);
+      return true;
+    }
+    if ((it & 255u) == 0 && give_up()) return false;
+  }
+}
+template <int C>
+__device__ __forceinline__ uint8_t* ll_line(uint8_t* llslot, uint64_t rel0) {
+  return llslot + 32 + (rel0 / CodecT<C>::E) * 32;
 }
 
 // Abort this call on every rank: peers' spins see it and stop waiting.
@@ -296,7 +344,7 @@ __device__ __forceinline__ float read_max_slot(Ctl* ctl, int idx) {
 
 }  // namespace
 
-template <int C>
+template <int C, bool LL>
 __device__ __forceinline__ void ring_body(const RingParams& P) {
   constexpr int E = CodecT<C>::E;
   const int G = P.G;
@@ -329,6 +377,56 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       }
     }
     return v;
+  };
+
+  // LL protocol state (ring.cuh:kLLBlock; never quant8): per-lane give-up
+  // flag for polls (1 = this rank's timeout, 2 = a peer aborted the call).
+  constexpr bool ll = LL && C != kQuant8;
+  uint64_t ll_t0 = 0;
+  int ll_fail = 0;
+  auto give_up = [&]() -> bool {
+    if (ll_fail) return true;
+    if (aborted(P, ctl)) {
+      ll_fail = 2;
+      return true;
+    }
+    const uint64_t now = globaltimer();
+    if (!ll_t0) ll_t0 = now;
+    else if (now - ll_t0 > P.timeout_ns) ll_fail = 1;
+    return ll_fail != 0;
+  };
+  auto ll_load = [&](const uint8_t* llslot, uint64_t rel0) -> uint4 {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (!ll_fail) ll_get(ll_line<C>(const_cast<uint8_t*>(llslot), rel0), v, give_up);
+    return v;
+  };
+  // chunk 0 carries the slot header line (collective.py:_expect, :52-64)
+  auto ll_hdr_put = [&](uint8_t* llslot, uint32_t c, int block, uint64_t len) {
+    if (c == 0 && lane_id() == 0) ll_put(llslot, make_uint4((uint32_t)block, P.iteration, (uint32_t)len, 0u));
+  };
+  // warp: any lane gave up -> latch like warp_await and leave
+  auto ll_ok = [&](int phase, int step, int block) -> bool {
+    const int any = __any_sync(0xffffffffu, ll_fail != 0), own = __any_sync(0xffffffffu, ll_fail == 1);
+    if (!any) return true;
+    if (lane_id() == 0) {
+      latch_error(err, kErrTimeout, phase, step, block, r, own ? 0 : 1);
+      if (own) broadcast_abort(P, R);
+    }
+    return false;
+  };
+  auto ll_hdr_get = [&](const uint8_t* llslot, uint32_t c, int phase, int step, int block, uint64_t len) -> bool {
+    int ok = 1;
+    if (c == 0 && lane_id() == 0) {
+      uint4 h;
+      if (ll_get(const_cast<uint8_t*>(llslot), h, give_up) &&
+          (h.x != (uint32_t)block || h.y != P.iteration || h.z != (uint32_t)len)) {
+        latch_error(err, kErrHeader, phase, step, block, r, (int)h.z);
+        broadcast_abort(P, R);
+        ok = 0;
+      }
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    return ok && ll_ok(phase, step, block);
   };
 
   // ---- reduce-scatter step 0, send side: C(x_r[block r]) -> succ slot 0
@@ -378,15 +476,19 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       stamp(P, wid, lr, 16);
     }
     uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
+    uint8_t* lld = ll_ptr(R.peer[succ], P.L, rs_slot(0));
     bool first0 = true;
     for (uint32_t c = grab(ctl, 1); c < B.nch; c = grab(ctl, 1)) {
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
-                      store_pay<C>(dst, g0 - B.A, vlo, vhi, encode_v<C>(px(v), q, bad));
+                      const uint4 pk = encode_v<C>(px(v), q, bad);
+                      if (ll) ll_put(ll_line<C>(lld, g0 - B.A), pk);
+                      else store_pay<C>(dst, g0 - B.A, vlo, vhi, pk);
                     });
       stamp2(P, wid, lr, 7, first0);
-      warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
+      if (ll) ll_hdr_put(lld, c, r, B.len);
+      else warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
       stamp2(P, wid, lr, 8, first0);
       first0 = false;
     }
@@ -403,15 +505,20 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const bool last = (s == p - 2);
     const uint8_t* in_slot = slot_ptr(R.inbox, P.L, rs_slot(s));
     uint8_t* fwd = last ? nullptr : slot_ptr(R.peer[succ], P.L, rs_slot(s + 1));
+    const uint8_t* ll_in = ll_ptr(R.inbox, P.L, rs_slot(s));
+    uint8_t* ll_fwd = last ? nullptr : ll_ptr(R.peer[succ], P.L, rs_slot(s + 1));
     auto load_xin = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-      return XIn<E>{load_fv<E>(x, g0, lo, hi), load_pay<C>(in_slot, g0 - B.A, vlo, vhi)};
+      return XIn<E>{load_fv<E>(x, g0, lo, hi), ll ? ll_load(ll_in, g0 - B.A) : load_pay<C>(in_slot, g0 - B.A, vlo, vhi)};
     };
     auto emit = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const uint4& pk, float sc) {
       if (!last) {
-        store_pay<C>(fwd, g0 - B.A, vlo, vhi, pk);
+        if (ll) ll_put(ll_line<C>(ll_fwd, g0 - B.A), pk);
+        else store_pay<C>(fwd, g0 - B.A, vlo, vhi, pk);
       } else {
-        for (int d = 1; d < p; ++d)
-          store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+        for (int d = 1; d < p; ++d) {
+          if (ll) ll_put(ll_line<C>(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A), pk);
+          else store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+        }
         if (own_via_inbox)
           store_pay<C>(slot_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
         else if (slot_mode)
@@ -421,6 +528,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       }
     };
     auto publish_last = [&](uint32_t c, float sc) {
+      if (ll) {
+        for (int d = 1; d < p; ++d) ll_hdr_put(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), c, b, B.len);
+        return;
+      }
       warp_publish_all(P, R, b, c, B.len, sc);
       if (own_via_inbox && lane_id() == 0) {
         if (c == 0) write_hdr(P, R.inbox, ag_slot(p, b), b, B.len, sc);
@@ -432,18 +543,27 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       const Q8 q = q8_make(0.f);
       bool first = true;
       for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
-        float sin;
+        float sin = 0.f;
         stamp2(P, wid, lr, 4, first);
-        if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
+        if (ll) {
+          if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len)) return;
+        } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
+          return;
+        }
         if (first) stamp(P, wid, lr, 2 + 2 * s);
         for_groups<C>(P, B, c, load_xin,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                         emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
                              0.f);
                       });
+        if (ll && !ll_ok(kPhRS, s, b)) return;
         stamp2(P, wid, lr, 5, first);
-        if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
-        else publish_last(c, 0.f);
+        if (!last) {
+          if (ll) ll_hdr_put(ll_fwd, c, b, B.len);
+          else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
+        } else {
+          publish_last(c, 0.f);
+        }
         stamp2(P, wid, lr, 6, first);
         first = false;
       }
@@ -523,16 +643,21 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const Blk B = get_blk(P, b);
     const int step = (r - b + p) % p;  // reference allgather step that delivers block b
     const uint8_t* in_slot = slot_ptr(R.inbox, P.L, ag_slot(p, b));
+    const uint8_t* ll_in = ll_ptr(R.inbox, P.L, ag_slot(p, b));
     bool first = true;
     for (uint32_t c = grab(ctl, 20 + k); c < B.nch; c = grab(ctl, 20 + k)) {
-      float sin;
+      float sin = 0.f;
       stamp2(P, wid, lr, 9, first && k == 1);
-      if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) return;
+      if (ll) {
+        if (!ll_hdr_get(ll_in, c, kPhAG, step, b, B.len)) return;
+      } else if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) {
+        return;
+      }
       if (k == 1 && first) stamp(P, wid, lr, 18);
       first = false;
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
-                      return load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
+                      return ll ? ll_load(ll_in, g0 - B.A) : load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
                     },
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const uint4& v) {
                       if (!slot_mode) {
@@ -543,6 +668,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                         store_pay<C>(R.slot, g0, vlo, vhi, v);
                       }
                     });
+      if (ll && !ll_ok(kPhAG, step, b)) return;
     }
   }
   stamp(P, wid, lr, 19);
@@ -551,14 +677,14 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
 #ifndef PIPESGD_RING_MINBLOCKS
 #define PIPESGD_RING_MINBLOCKS (2048 / kRingThreads / 4 > 0 ? 2048 / kRingThreads / 4 : 1)
 #endif
-template <int C>
+template <int C, bool LL>
 __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
   if (threadIdx.x == 0) s_seq = (uint32_t)(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)) + 1);
   __syncthreads();
-  ring_body<C>(P);  // returns early (per warp) on timeout / abort / header mismatch
+  ring_body<C, LL>(P);  // returns early (per warp) on timeout / abort / header mismatch
   // Last warp of this rank to leave closes the call: counters reset, calls
   // advanced. The next call on this stream starts only after this kernel.
   __syncwarp();
@@ -577,9 +703,13 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
 void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError_t* err) {
   void* args[] = {const_cast<RingParams*>(&P)};
   const dim3 grid(P.G * nlocal), block(kRingThreads);
-  const void* fn = P.codec == kNone      ? (const void*)ring_allreduce_kernel<kNone>
-                   : P.codec == kTrunc16 ? (const void*)ring_allreduce_kernel<kTrunc16>
-                                         : (const void*)ring_allreduce_kernel<kQuant8>;
+  const void* fn = P.codec == kNone
+                       ? (P.ll ? (const void*)ring_allreduce_kernel<kNone, true>
+                               : (const void*)ring_allreduce_kernel<kNone, false>)
+                   : P.codec == kTrunc16
+                       ? (P.ll ? (const void*)ring_allreduce_kernel<kTrunc16, true>
+                               : (const void*)ring_allreduce_kernel<kTrunc16, false>)
+                       : (const void*)ring_allreduce_kernel<kQuant8, false>;
   // Emulated rings (nlocal > 1) need every CTA co-resident: cooperative
   // launch. A single rank per GPU only needs its G <= #SM CTAs to become
   // resident eventually (no CTA waits on a CTA of its own launch except the
@@ -600,8 +730,11 @@ int ring_warps_per_cta() { return kWarps; }
 
 int ring_max_ctas_per_sm() {
   int m = 1 << 30;
-  const void* fns[3] = {(const void*)ring_allreduce_kernel<kNone>, (const void*)ring_allreduce_kernel<kTrunc16>,
-                        (const void*)ring_allreduce_kernel<kQuant8>};
+  const void* fns[5] = {(const void*)ring_allreduce_kernel<kNone, false>,
+                        (const void*)ring_allreduce_kernel<kTrunc16, false>,
+                        (const void*)ring_allreduce_kernel<kQuant8, false>,
+                        (const void*)ring_allreduce_kernel<kNone, true>,
+                        (const void*)ring_allreduce_kernel<kTrunc16, true>};
   for (const void* f : fns) {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, kRingThreads, 0);

@@ -16,9 +16,23 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 
 // Per-rank inbox layout (identical on every rank of a communicator). Peers
 // write payload, headers and flags here over NVLink; ctl/err are private.
+// Low-latency (LL) protocol for small blocks: every 8-byte word carries 4
+// payload bytes and the call's sequence number, so a receiver polls the data
+// itself and no release fence / flag store is needed. Blocks of at most
+// kLLBlock elements (none / trunc16) take it; compile-time so that every rank
+// makes the same choice.
+#ifndef PIPESGD_LL_BLOCK
+#define PIPESGD_LL_BLOCK 16384
+#endif
+constexpr uint64_t kLLBlock = PIPESGD_LL_BLOCK;
+constexpr uint64_t kLLRegionBlock = 65536;  // LL slot capacity (elements), fixed so layouts agree
+
 struct Layout {
   uint64_t off_ctl, off_err, off_hdr, off_flags, off_payload;
   uint64_t slot_bytes;   // payload bytes per slot
+  uint64_t off_ll;       // LL region: nslot x ll_slot_bytes (32-byte header line + 2 x 16 B per group)
+  uint64_t ll_slot_bytes;
+  uint64_t ll_max_blk;   // largest block (elements) an LL slot holds
   uint64_t total_bytes;
   uint32_t max_chunks;   // flags per slot
   uint32_t nslot;        // 2p-1: p-1 reduce-scatter slots + p allgather slots
@@ -58,6 +72,7 @@ struct RingParams {
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
   int p, codec, G;             // world size, codec tag, CTAs per rank (16 warp workers each)
   int pre;                     // x is the raw gradient: apply the local D(C(.)) on load
+  int ll;                      // this call uses the LL protocol (see kLLBlock)
   unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
 

@@ -212,3 +212,40 @@ def test_p2p_ring_in_cuda_graph_replays_bit_exact(P):
                     assert_bits_equal(rep[c], want[c], f"rank {r} {c.name}")
     finally:
         tr.close()
+
+
+@multigpu
+@pytest.mark.parametrize("n", [8, 300_007])  # LL protocol / flag protocol
+def test_p2p_iteration_tag_mismatch_is_a_header_error(P, n):
+    """collective.py:52-64: a block carrying another iteration tag is rejected
+    (both wire protocols validate the slot header with chunk 0)."""
+    tr = P.GpuTransport(2, timeout_s=5.0, max_elems=n)
+    try:
+        xs = [torch.ones(n, device=f"cuda:{r}") for r in range(2)]
+        with pytest.raises(P.CollectiveError, match="iteration tag"):
+            run_ranks(tr, lambda r, ep: P.ring_allreduce(xs[r], r, 2, ep, P.Codec.TRUNC16, iteration=1 + r))
+    finally:
+        tr.close()
+
+
+@multigpu
+def test_p2p_ll_threshold_and_protocol_switching(P):
+    """Sizes either side of the LL threshold (blocks of <= 16384 elements use
+    the sequence-tagged LL slots, larger ones the flag protocol), called
+    alternately on one communicator: every result equals the reference's, so
+    neither protocol ever reads the other's stale bytes."""
+    p = 2
+    sizes = [8, 2 * 16368 - 1, 2 * 16368, 2 * 16368 + 1, 2 * 16368 + 33, 100_003, 8, 2 * 16368, 5]
+    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=max(sizes))
+    try:
+        for k, n in enumerate(sizes):
+            g = np.random.default_rng(k)
+            ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
+            for codec in P.Codec:
+                want = OR.ring_allreduce_all(ins, int(codec)).outputs[0]
+                xs = [torch.from_numpy(v).to(f"cuda:{r}") for r, v in enumerate(ins)]
+                res = run_ranks(tr, lambda r, ep: P.ring_allreduce(xs[r], r, p, ep, codec, iteration=k))
+                for r, y in enumerate(res):
+                    assert_bits_equal(y.cpu().numpy(), want, f"n={n} {codec.name} rank {r}")
+    finally:
+        tr.close()
