@@ -52,7 +52,7 @@ Layout make_layout(int p, uint64_t max_elems) {
   L.off_hdr = 4096 + 256;
   L.off_flags = round_up(L.off_hdr + (uint64_t)L.nslot * sizeof(SlotHdr), 256);
   L.off_payload = round_up(L.off_flags + (uint64_t)L.nslot * L.max_chunks * 8, 4096);
-  L.ll_max_blk = std::min<uint64_t>(maxblk, kLLRegionBlock);
+  L.ll_max_blk = std::min<uint64_t>(maxblk + 16, kLLRegionBlock);  // + the launch's alignment slack
   L.ll_slot_bytes = round_up(32 + 8 * (L.ll_max_blk + 32), 256);  // worst case fp32: 8 B per element
   L.off_ll = L.off_payload + (uint64_t)L.nslot * L.slot_bytes;
   L.total_bytes = L.off_ll + (uint64_t)L.nslot * L.ll_slot_bytes;

@@ -19,13 +19,16 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 // Low-latency (LL) protocol for small blocks: every 8-byte word carries 4
 // payload bytes and the call's sequence number, so a receiver polls the data
 // itself and no release fence / flag store is needed. Blocks of at most
-// kLLBlock elements (none / trunc16) take it; compile-time so that every rank
-// makes the same choice.
+// kLLBlock elements (none / trunc16; including the 16-element alignment
+// slack) take it; compile-time so that every rank makes the same choice.
 #ifndef PIPESGD_LL_BLOCK
-#define PIPESGD_LL_BLOCK 16384
+#define PIPESGD_LL_BLOCK 262144  // A/B: profiles/r01_c5/ll_threshold_ab.log
 #endif
 constexpr uint64_t kLLBlock = PIPESGD_LL_BLOCK;
-constexpr uint64_t kLLRegionBlock = 65536;  // LL slot capacity (elements), fixed so layouts agree
+#ifndef PIPESGD_LL_REGION
+#define PIPESGD_LL_REGION 262144
+#endif
+constexpr uint64_t kLLRegionBlock = PIPESGD_LL_REGION;  // LL slot capacity (elements), fixed so layouts agree
 
 struct Layout {
   uint64_t off_ctl, off_err, off_hdr, off_flags, off_payload;
