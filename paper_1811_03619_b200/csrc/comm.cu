@@ -52,8 +52,10 @@ Layout make_layout(int p, uint64_t max_elems) {
   L.off_hdr = 4096 + 256;
   L.off_flags = round_up(L.off_hdr + (uint64_t)L.nslot * sizeof(SlotHdr), 256);
   L.off_payload = round_up(L.off_flags + (uint64_t)L.nslot * L.max_chunks * 8, 4096);
-  L.ll_max_blk = std::min<uint64_t>(maxblk + 16, kLLRegionBlock);  // + the launch's alignment slack
-  L.ll_slot_bytes = round_up(32 + 8 * (L.ll_max_blk + 32), 256);  // worst case fp32: 8 B per element
+  // LL slot: a 32-byte header line + 2 x the payload of the largest block
+  // (+ the launch's 16-element slack, fp32 worst case) up to kLLRegionBytes
+  L.ll_cap = std::min<uint64_t>(4 * (maxblk + 16), kLLRegionBytes);
+  L.ll_slot_bytes = round_up(32 + 2 * (L.ll_cap + 4 * 32), 256);
   L.off_ll = L.off_payload + (uint64_t)L.nslot * L.slot_bytes;
   L.total_bytes = L.off_ll + (uint64_t)L.nslot * L.ll_slot_bytes;
   return L;
@@ -374,7 +376,8 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
     uint64_t nch = (maxblk + P.chunk - 1) / P.chunk;
     if (P.pre && codec == GP_CODEC_QUANT8) nch = std::max<uint64_t>(nch, (n + P.chunk - 1) / P.chunk);
     P.G = (int)std::min<uint64_t>((uint64_t)c->G, std::max<uint64_t>(1, (nch + kRingWarps - 1) / kRingWarps));
-    P.ll = (codec != GP_CODEC_QUANT8 && maxblk <= std::min<uint64_t>(kLLBlock, c->L.ll_max_blk)) ? 1 : 0;
+    const uint64_t w = codec == GP_CODEC_NONE ? 4 : 2;
+    P.ll = (codec != GP_CODEC_QUANT8 && maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), c->L.ll_cap)) ? 1 : 0;
   }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;

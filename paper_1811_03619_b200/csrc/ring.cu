@@ -77,7 +77,7 @@ __device__ __forceinline__ uint8_t* slot_ptr(uint8_t* inbox, const Layout& L, in
   return inbox + L.off_payload + (uint64_t)slot * L.slot_bytes;
 }
 
-// ---- LL protocol (small blocks, ring.cuh:kLLBlock). A slot is a 32-byte
+// ---- LL protocol (small blocks, ring.cuh:ll_payload_limit). A slot is a 32-byte
 // header line then one 32-byte line per 16-byte payload group; every 8-byte
 // word is {4 payload bytes, call sequence}, written with one 16-byte volatile
 // store per half line. Aligned 8-byte accesses are single-copy atomic, so a
@@ -379,7 +379,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     return v;
   };
 
-  // LL protocol state (ring.cuh:kLLBlock; never quant8): per-lane give-up
+  // LL protocol state (ring.cuh:ll_payload_limit; never quant8): per-lane give-up
   // flag for polls (1 = this rank's timeout, 2 = a peer aborted the call).
   constexpr bool ll = LL && C != kQuant8;
   uint64_t ll_t0 = 0;

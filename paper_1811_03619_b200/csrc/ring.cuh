@@ -18,24 +18,32 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 // write payload, headers and flags here over NVLink; ctl/err are private.
 // Low-latency (LL) protocol for small blocks: every 8-byte word carries 4
 // payload bytes and the call's sequence number, so a receiver polls the data
-// itself and no release fence / flag store is needed. Blocks of at most
-// kLLBlock elements (none / trunc16; including the 16-element alignment
-// slack) take it; compile-time so that every rank makes the same choice.
-#ifndef PIPESGD_LL_BLOCK
-#define PIPESGD_LL_BLOCK 262144  // A/B: profiles/r01_c5/ll_threshold_ab.log
+// itself and no release fence / flag store is needed, at twice the bytes.
+// A none/trunc16 call takes it when its block payload (elements incl. the
+// 16-element alignment slack x wire width) is at most kLLHopBytes x (p - 1):
+// every further hop saves one more fence (measured crossover: 512 KB at
+// p = 2, >= 1 MB at p = 4; profiles/r01_c5/ll_threshold_ab.log). Compile-time
+// constants, so every rank makes the same choice.
+#ifndef PIPESGD_LL_HOP_BYTES
+#define PIPESGD_LL_HOP_BYTES (512u << 10)
 #endif
-constexpr uint64_t kLLBlock = PIPESGD_LL_BLOCK;
-#ifndef PIPESGD_LL_REGION
-#define PIPESGD_LL_REGION 262144
+#ifndef PIPESGD_LL_REGION_BYTES
+#define PIPESGD_LL_REGION_BYTES (2u << 20)
 #endif
-constexpr uint64_t kLLRegionBlock = PIPESGD_LL_REGION;  // LL slot capacity (elements), fixed so layouts agree
+constexpr uint64_t kLLHopBytes = PIPESGD_LL_HOP_BYTES;
+constexpr uint64_t kLLRegionBytes = PIPESGD_LL_REGION_BYTES;  // largest LL block payload (fixed: layouts agree)
+
+__host__ __device__ inline uint64_t ll_payload_limit(int p) {
+  const uint64_t v = kLLHopBytes * (uint64_t)(p > 1 ? p - 1 : 1);
+  return v < kLLRegionBytes ? v : kLLRegionBytes;
+}
 
 struct Layout {
   uint64_t off_ctl, off_err, off_hdr, off_flags, off_payload;
   uint64_t slot_bytes;   // payload bytes per slot
   uint64_t off_ll;       // LL region: nslot x ll_slot_bytes (32-byte header line + 2 x 16 B per group)
   uint64_t ll_slot_bytes;
-  uint64_t ll_max_blk;   // largest block (elements) an LL slot holds
+  uint64_t ll_cap;       // largest block payload (bytes, incl. alignment slack) an LL slot holds
   uint64_t total_bytes;
   uint32_t max_chunks;   // flags per slot
   uint32_t nslot;        // 2p-1: p-1 reduce-scatter slots + p allgather slots
@@ -75,7 +83,7 @@ struct RingParams {
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
   int p, codec, G;             // world size, codec tag, CTAs per rank (16 warp workers each)
   int pre;                     // x is the raw gradient: apply the local D(C(.)) on load
-  int ll;                      // this call uses the LL protocol (see kLLBlock)
+  int ll;                      // this call uses the LL protocol (see ll_payload_limit)
   unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
 
