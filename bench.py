@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--mode", default="pipe_sgd")
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--global-batch", type=int, default=512)
-    ap.add_argument("--ctas", type=int, default=128,
+    ap.add_argument("--ctas", type=int, default=256,
                     help="128-thread CTAs the ring kernel may occupy per GPU beside the compute stream")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
@@ -550,7 +550,7 @@ def our_arm(args, ws, rank, local):
                 "kernel": roof["kernel"], "n": big["n"], "bound": "nvlink", "achieved": ach,
                 "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "ctas": FULL_CTAS,
                 "note": "the same ring kernel alone on a 256 MiB fp32 bucket with every SM (standalone "
-                        "allreduce configuration); the engine runs it on 128 CTAs beside the CNN"}
+                        "allreduce configuration); the engine runs it on %d CTAs beside the CNN" % args.ctas}
         line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms)
     return line
 

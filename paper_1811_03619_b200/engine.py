@@ -641,12 +641,12 @@ class RankEngine:
 
 # ----------------------------------------------------------------- clusters
 
-# CTAs (128 threads each, 512 warps in total) the ring kernel may occupy
+# CTAs (128 threads each, 1024 warps in total) the ring kernel may occupy
 # while the compute stream runs the next iteration; they share SMs with the
-# forward/backward kernels. The ring reaches ~300-530 GB/s at this budget on
-# 2xB200 (profiles/r01_ring_ctas_ab.log), far above what a pipelined step needs
-# to stay compute-bound.
-COMM_CTAS = 128
+# forward/backward kernels. Iterations/s do not depend on it between 32 and
+# 256 CTAs (the ring stays hidden: profiles/r01_ring_latency/comm_ctas_ab.log);
+# 256 gives the shortest ring inside the step (C2, N=2: 64 us vs 76 us at 128).
+COMM_CTAS = 256
 
 
 def _make_transport(workers: int, timeout_s: float, max_elems: int, ctas: int = COMM_CTAS):
