@@ -95,6 +95,10 @@ int gp_comm_set_tuning(gp_comm* comm, int ctas_per_rank, double timeout_s);
 int gp_comm_set_trace(gp_comm* comm, void* device_buffer);
 int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, emulated] */);
 int gp_comm_destroy(gp_comm* comm);
+/* Test hook: set the device call counter of this communicator's inbox(es)
+ * (sequence numbers cycle 1 .. 2^32-1; tests start near the wrap). Every rank
+ * must set the same value while no call is in flight. */
+int gp_comm_set_call_counter(gp_comm* comm, uint64_t calls);
 
 int gp_allreduce(gp_comm* comm, const float* in, float* out, uint64_t n, int codec,
                  uint32_t iteration, void* stream);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <string>
 
@@ -304,6 +305,19 @@ int gp_comm_info(gp_comm* c, int64_t* o) {
   if (!c || !o) return fail(GP_ERR_ARG, "null argument");
   o[0] = c->rank; o[1] = c->world; o[2] = c->device; o[3] = (int64_t)c->max_elems;
   o[4] = c->G; o[5] = (int64_t)c->L.total_bytes; o[6] = c->seq; o[7] = c->nlocal > 1;
+  return GP_OK;
+}
+
+int gp_comm_set_call_counter(gp_comm* c, uint64_t calls) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  if (calls > 0xFFFFFFFFull) return fail(GP_ERR_ARG, "call counter holds a 32-bit sequence number");
+  DeviceGuard g(c->device);
+  for (int i = 0; i < c->nlocal; ++i) {
+    const unsigned long long v = calls;
+    cudaError_t e = cudaMemcpy(c->inbox[i] + c->L.off_ctl + offsetof(Ctl, calls), &v, sizeof(v),
+                               cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "set call counter");
+  }
   return GP_OK;
 }
 

@@ -126,13 +126,13 @@ __device__ __forceinline__ uint8_t* ll_line(uint8_t* llslot, uint64_t rel0) {
 __device__ void broadcast_abort(const RingParams& P, const RankCtx& R) {
   for (int q = 0; q < P.p; ++q) {
     Ctl* c = reinterpret_cast<Ctl*>(R.peer[q] + P.L.off_ctl);
-    atomicMax(&c->abort, (unsigned long long)s_seq);
+    atomicExch(&c->abort, (unsigned long long)s_seq);
   }
   fence_sys();
 }
 
 __device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
-  return *(volatile unsigned long long*)&ctl->abort >= s_seq;
+  return (uint32_t)(*(volatile unsigned long long*)&ctl->abort) == s_seq;
 }
 
 // Flag word: (call sequence << 32) | quant8 scale bits. Carrying the scale in
@@ -147,13 +147,12 @@ __device__ __forceinline__ uint64_t flag_word(float scale) {
 // tight loop would flood L2), then takes the acquire with one ld.acquire.
 __device__ uint64_t spin_flag(const uint64_t* f, const RingParams& P, const RankCtx& R, Ctl* ctl,
                               ErrWord* err, int phase, int step, int block) {
-  const uint64_t want = (uint64_t)s_seq << 32;
   uint64_t v = ld_acquire_sys(f);
-  if (v >= want) return v;
+  if ((uint32_t)(v >> 32) == s_seq) return v;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
   for (uint32_t it = 1;; ++it) {
-    if (ld_relaxed_sys(f) >= want) return ld_acquire_sys(f);
+    if ((uint32_t)(ld_relaxed_sys(f) >> 32) == s_seq) return ld_acquire_sys(f);
     __nanosleep(ns);
     if (ns < 256) ns <<= 1;
     if ((it & 63u) == 0) {
@@ -682,7 +681,7 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
-  if (threadIdx.x == 0) s_seq = (uint32_t)(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)) + 1);
+  if (threadIdx.x == 0) s_seq = next_seq(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)));
   __syncthreads();
   ring_body<C, LL>(P);  // returns early (per warp) on timeout / abort / header mismatch
   // Last warp of this rank to leave closes the call: counters reset, calls
@@ -694,6 +693,7 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
       ctl->exits = 0;
       ctl->bar = 0;
       for (int i = 0; i < 32; ++i) ctl->next[i] = 0;
+      for (int i = 0; i < 16; ++i) ctl->maxslot[i] = 0;
       __threadfence();
       atomicExch(&ctl->calls, (unsigned long long)s_seq);
     }

@@ -49,14 +49,23 @@ struct Layout {
   uint32_t nslot;        // 2p-1: p-1 reduce-scatter slots + p allgather slots
 };
 
-struct Ctl {                   // rank-private control block
+struct Ctl {                   // rank-private control block (peers write abort / ack)
   unsigned long long bar;      // quant8 barrier arrivals in the current call
-  unsigned long long abort;    // >= seq when the current call aborted
-  unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier
-  unsigned long long calls;    // completed calls; this call's sequence number is calls + 1
+  unsigned long long abort;    // == seq when the current call aborted
+  unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier (reset per call)
+  unsigned long long calls;    // sequence number of the last completed call
   unsigned long long exits;    // warps that finished the current call
   unsigned long long next[32]; // per-phase chunk counters (dynamic chunk scheduling)
+  unsigned long long ack[kMaxRanks];  // star calls: == seq once rank q consumed this rank's data
 };
+
+// Call sequence numbers cycle through 1 .. 2^32 - 1: never 0 (the value of
+// zero-initialised flags and LL words), and every check compares for
+// equality, so the 32-bit counter may wrap (a rank is never more than one
+// call ahead of the data it reads).
+__host__ __device__ inline uint32_t next_seq(unsigned long long calls) {
+  return (uint32_t)(calls % 0xFFFFFFFFull) + 1u;
+}
 
 struct SlotHdr {               // written by the sender before each chunk flag
   uint32_t seq, iteration, block, n_elems;

@@ -57,19 +57,18 @@ __device__ __forceinline__ float* staged(uint8_t* inbox, const Layout& L) {
 
 __device__ bool star_wait(const uint64_t* f, const StarParams& P, Ctl* ctl, ErrWord* err, int phase, int src,
                           int rank) {
-  const uint64_t want = (uint64_t)s_star_seq << 32;
-  if (ld_acquire_sys(f) >= want) return true;
+  if ((uint32_t)(ld_acquire_sys(f) >> 32) == s_star_seq) return true;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 64;
   for (uint32_t it = 1;; ++it) {
-    if (ld_relaxed_sys(f) >= want) {
+    if ((uint32_t)(ld_relaxed_sys(f) >> 32) == s_star_seq) {
       (void)ld_acquire_sys(f);
       return true;
     }
     __nanosleep(ns);
     if (ns < 512) ns <<= 1;
     if ((it & 31u) == 0) {
-      if (*(volatile unsigned long long*)&ctl->abort >= s_star_seq) {
+      if ((uint32_t)(*(volatile unsigned long long*)&ctl->abort) == s_star_seq) {
         latch_error(err, kErrTimeout, phase, 0, src, rank, 1);
         return false;
       }
@@ -213,16 +212,55 @@ __device__ void star_body(const StarParams& P) {
   }
 }
 
+// Lane 0: wait until ack word `a` carries this call's sequence.
+__device__ bool star_wait_ack(unsigned long long* a, const StarParams& P, Ctl* ctl, ErrWord* err, int phase,
+                              int src, int rank) {
+  return star_wait(reinterpret_cast<const uint64_t*>(a), P, ctl, err, phase, src, rank);
+}
+
+// Close of a star call, run by the last warp of a rank: the side whose
+// staged bytes were read waits until every reader acknowledged, so a rank
+// never restages (next call) over data a peer is still reading.
+//   gather:    the root, done folding, acks every source; sources wait.
+//   broadcast: every receiver, done pulling, acks the root; the root waits.
+__device__ void star_close_handshake(const StarParams& P, const StarRank& R, Ctl* ctl) {
+  if (P.p < 2) return;
+  ErrWord* err = reinterpret_cast<ErrWord*>(R.inbox + P.L.off_err);
+  const int phase = P.mode == 0 ? kPhRS : kPhAG;
+  const bool root = R.rank == P.root;
+  const uint64_t ackw = (uint64_t)s_star_seq << 32;
+  auto peer_ctl = [&](int q) { return reinterpret_cast<Ctl*>(R.peer[q] + P.L.off_ctl); };
+  if (P.mode == 0) {
+    if (root) {
+      __threadfence_system();
+      for (int q = 0; q < P.p; ++q)
+        if (q != R.rank) st_release_sys(reinterpret_cast<uint64_t*>(&peer_ctl(q)->ack[R.rank]), ackw);
+    } else {
+      star_wait_ack(&ctl->ack[P.root], P, ctl, err, phase, P.root, R.rank);
+    }
+  } else {
+    if (!root) {
+      __threadfence_system();
+      st_release_sys(reinterpret_cast<uint64_t*>(&peer_ctl(P.root)->ack[R.rank]), ackw);
+    } else {
+      for (int q = 0; q < P.p; ++q)
+        if (q != R.rank && !star_wait_ack(&ctl->ack[q], P, ctl, err, phase, q, R.rank)) break;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kStarThreads) star_kernel(const __grid_constant__ StarParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
-  if (threadIdx.x == 0) s_star_seq = (uint32_t)(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)) + 1);
+  if (threadIdx.x == 0) s_star_seq = next_seq(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)));
   __syncthreads();
   star_body(P);
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {  // last warp of this rank closes the call (as the ring does)
     const unsigned long long prev = atomicAdd(&ctl->exits, 1ull);
     if (prev == (unsigned long long)P.G * kStarWarps - 1) {
+      __threadfence();  // every warp of this rank is done with the staged data
+      star_close_handshake(P, P.rk[lr], ctl);
       ctl->exits = 0;
       for (int i = 0; i < 32; ++i) ctl->next[i] = 0;
       __threadfence();

@@ -208,3 +208,35 @@ def test_star_collectives_match_reference_semantics(P):
             assert o.tobytes() == value.tobytes()
     finally:
         tr.close()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_star_back_to_back_over_nvlink_across_sequence_wrap(P):
+    """Real per-GPU launches (no shared cooperative launch): back-to-back
+    gathers with changing roots and back-to-back broadcasts stay exact,
+    because a star call closes only once every reader acknowledged the
+    staged bytes; started two calls before the 32-bit call sequence wraps."""
+    from helpers import run_ranks
+    from paper_1811_03619_b200 import _lib
+    from paper_1811_03619_b200.collective import broadcast_from_root, gather_to_root
+    p = min(torch.cuda.device_count(), 4)
+    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=1 << 20)
+    try:
+        for r in range(p):
+            _lib.call("gp_comm_set_call_counter", tr.endpoint(r)._comm, 0xFFFFFFFF - 2)
+        g = np.random.default_rng(9)
+        for it in range(6):
+            ins = [g.normal(0, 1, 700_001).astype(np.float32) for _ in range(p)]
+            root = it % p
+            outs = run_ranks(tr, lambda r, ep: gather_to_root(ins[r], root, r, p, ep))
+            want = ins[root].copy()
+            for s in range(p):
+                if s != root:
+                    want = want + ins[s]
+            assert_bits_equal(outs[root], want, f"gather {it} root {root}")
+            value = g.normal(0, 1, 500_000 + it).astype(np.float32)
+            outs = run_ranks(tr, lambda r, ep: broadcast_from_root(value if r == root else None, root, r, p, ep))
+            for o in outs:
+                assert o.tobytes() == value.tobytes()
+    finally:
+        tr.close()

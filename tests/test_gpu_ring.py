@@ -251,3 +251,28 @@ def test_p2p_ll_threshold_and_protocol_switching(P):
                     assert_bits_equal(y.cpu().numpy(), want, f"n={n} {codec.name} rank {r}")
     finally:
         tr.close()
+
+
+@multigpu
+def test_p2p_ring_across_call_sequence_wrap(P):
+    """Sequence numbers cycle 1 .. 2^32-1 and every check is an equality:
+    calls straddling the wrap (both wire protocols, every codec, fused
+    variants included via the graph test's allreduce_into path) stay exact."""
+    from paper_1811_03619_b200 import _lib
+    p = 2
+    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=300_007)
+    try:
+        for r in range(p):
+            _lib.call("gp_comm_set_call_counter", tr.endpoint(r)._comm, 0xFFFFFFFF - 4)
+        for k in range(4):
+            for n in (1000, 300_007):  # LL / flag protocol
+                g = np.random.default_rng(100 * k + n % 7)
+                ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
+                for codec in P.Codec:
+                    want = OR.ring_allreduce_all(ins, int(codec)).outputs[0]
+                    xs = [torch.from_numpy(v).to(f"cuda:{r}") for r, v in enumerate(ins)]
+                    res = run_ranks(tr, lambda r, ep: P.ring_allreduce(xs[r], r, p, ep, codec, iteration=k))
+                    for r, y in enumerate(res):
+                        assert_bits_equal(y.cpu().numpy(), want, f"k={k} n={n} {codec.name} rank {r}")
+    finally:
+        tr.close()
