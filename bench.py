@@ -546,9 +546,14 @@ def our_arm(args, ws, rank, local):
             wire_big = 2 * (N - 1) / N * big["n"] * w
             key = f"{args.codec}@{FULL_CTAS}ctas"
             ach = wire_big / (big[key]["ms"] * 1e-3) / 1e9
+            none_key = f"none@{FULL_CTAS}ctas"
+            none_gbs = (2 * (N - 1) / N * 4 * big["n"] / (big[none_key]["ms"] * 1e-3) / 1e9
+                        if none_key in big else None)
             line["roofline_large_bucket"] = {
                 "kernel": roof["kernel"], "n": big["n"], "bound": "nvlink", "achieved": ach,
                 "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": ach / NVLINK_PEAK_GBS, "ctas": FULL_CTAS,
+                "codec_none_busbw_gbs": none_gbs,
+                "codec_none_frac": none_gbs / NVLINK_PEAK_GBS if none_gbs else None,
                 "note": "the same ring kernel alone on a 256 MiB fp32 bucket with every SM (standalone "
                         "allreduce configuration); the engine runs it on %d CTAs beside the CNN" % args.ctas}
         line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms)
@@ -669,6 +674,8 @@ def ring_vs_nccl(ep, codec, N, dev, sizes, ctas_list=(0,)):
             s.synchronize()
             dist.barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                torch.cuda._sleep(2_000_000)  # host enqueues the series before the clock starts
             a.record(s)
             for _ in range(it):
                 run()
