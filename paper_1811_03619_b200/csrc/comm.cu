@@ -390,8 +390,8 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
     uint64_t nch = (maxblk + P.chunk - 1) / P.chunk;
     if (P.pre && codec == GP_CODEC_QUANT8) nch = std::max<uint64_t>(nch, (n + P.chunk - 1) / P.chunk);
     P.G = (int)std::min<uint64_t>((uint64_t)c->G, std::max<uint64_t>(1, (nch + kRingWarps - 1) / kRingWarps));
-    const uint64_t w = codec == GP_CODEC_NONE ? 4 : 2;
-    P.ll = (codec != GP_CODEC_QUANT8 && maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), c->L.ll_cap)) ? 1 : 0;
+    const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
+    P.ll = (maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), c->L.ll_cap)) ? 1 : 0;
   }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;

@@ -378,9 +378,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     return v;
   };
 
-  // LL protocol state (ring.cuh:ll_payload_limit; never quant8): per-lane give-up
-  // flag for polls (1 = this rank's timeout, 2 = a peer aborted the call).
-  constexpr bool ll = LL && C != kQuant8;
+  // LL protocol state (ring.cuh:ll_payload_limit): per-lane give-up flag for
+  // polls (1 = this rank's timeout, 2 = a peer aborted the call). quant8's
+  // block scale travels in the header line's 4th word (not in flags).
+  constexpr bool ll = LL;
   uint64_t ll_t0 = 0;
   int ll_fail = 0;
   auto give_up = [&]() -> bool {
@@ -400,8 +401,9 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     return v;
   };
   // chunk 0 carries the slot header line (collective.py:_expect, :52-64)
-  auto ll_hdr_put = [&](uint8_t* llslot, uint32_t c, int block, uint64_t len) {
-    if (c == 0 && lane_id() == 0) ll_put(llslot, make_uint4((uint32_t)block, P.iteration, (uint32_t)len, 0u));
+  auto ll_hdr_put = [&](uint8_t* llslot, uint32_t c, int block, uint64_t len, float scale) {
+    if (c == 0 && lane_id() == 0)
+      ll_put(llslot, make_uint4((uint32_t)block, P.iteration, (uint32_t)len, __float_as_uint(scale)));
   };
   // warp: any lane gave up -> latch like warp_await and leave
   auto ll_ok = [&](int phase, int step, int block) -> bool {
@@ -413,18 +415,23 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     }
     return false;
   };
-  auto ll_hdr_get = [&](const uint8_t* llslot, uint32_t c, int phase, int step, int block, uint64_t len) -> bool {
+  auto ll_hdr_get = [&](const uint8_t* llslot, uint32_t c, int phase, int step, int block, uint64_t len,
+                        float& scale) -> bool {
     int ok = 1;
-    if (c == 0 && lane_id() == 0) {
+    uint32_t sb = 0;
+    if ((c == 0 || C == kQuant8) && lane_id() == 0) {
       uint4 h;
-      if (ll_get(const_cast<uint8_t*>(llslot), h, give_up) &&
-          (h.x != (uint32_t)block || h.y != P.iteration || h.z != (uint32_t)len)) {
-        latch_error(err, kErrHeader, phase, step, block, r, (int)h.z);
-        broadcast_abort(P, R);
-        ok = 0;
+      if (ll_get(const_cast<uint8_t*>(llslot), h, give_up)) {
+        sb = h.w;
+        if (c == 0 && (h.x != (uint32_t)block || h.y != P.iteration || h.z != (uint32_t)len)) {
+          latch_error(err, kErrHeader, phase, step, block, r, (int)h.z);
+          broadcast_abort(P, R);
+          ok = 0;
+        }
       }
     }
     ok = __shfl_sync(0xffffffffu, ok, 0);
+    scale = __uint_as_float(__shfl_sync(0xffffffffu, sb, 0));
     return ok && ll_ok(phase, step, block);
   };
 
@@ -486,7 +493,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                       else store_pay<C>(dst, g0 - B.A, vlo, vhi, pk);
                     });
       stamp2(P, wid, lr, 7, first0);
-      if (ll) ll_hdr_put(lld, c, r, B.len);
+      if (ll) ll_hdr_put(lld, c, r, B.len, q.s);
       else warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
       stamp2(P, wid, lr, 8, first0);
       first0 = false;
@@ -518,9 +525,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           if (ll) ll_put(ll_line<C>(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A), pk);
           else store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
         }
-        if (own_via_inbox)
-          store_pay<C>(slot_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
-        else if (slot_mode)
+        if (own_via_inbox) {
+          if (ll) ll_put(ll_line<C>(ll_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A), pk);
+          else store_pay<C>(slot_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+        } else if (slot_mode)
           store_pay<C>(R.slot, g0, vlo, vhi, pk);  // none/trunc16: C(D(wire)) == wire
         else
           store_fv<E>(out, g0, lo, hi, decode_v<C>(pk, sc));
@@ -528,7 +536,8 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     };
     auto publish_last = [&](uint32_t c, float sc) {
       if (ll) {
-        for (int d = 1; d < p; ++d) ll_hdr_put(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), c, b, B.len);
+        for (int d = 1; d < p; ++d) ll_hdr_put(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), c, b, B.len, sc);
+        if (own_via_inbox) ll_hdr_put(ll_ptr(R.inbox, P.L, ag_slot(p, b)), c, b, B.len, sc);
         return;
       }
       warp_publish_all(P, R, b, c, B.len, sc);
@@ -545,7 +554,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         float sin = 0.f;
         stamp2(P, wid, lr, 4, first);
         if (ll) {
-          if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len)) return;
+          if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
         } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
           return;
         }
@@ -558,7 +567,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         if (ll && !ll_ok(kPhRS, s, b)) return;
         stamp2(P, wid, lr, 5, first);
         if (!last) {
-          if (ll) ll_hdr_put(ll_fwd, c, b, B.len);
+          if (ll) ll_hdr_put(ll_fwd, c, b, B.len, 0.f);
           else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
         } else {
           publish_last(c, 0.f);
@@ -572,7 +581,11 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       bool first = true;
       for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
         float sin;
-        if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) return;
+        if (ll) {
+          if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
+        } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
+          return;
+        }
         if (first) stamp(P, wid, lr, 2 + 2 * s);
         first = false;
         for_groups<C>(P, B, c, load_xin,
@@ -581,6 +594,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                         m = max(m, absmax_bits(acc));
                         store_fv<E>(out, g0, lo, hi, acc);
                       });
+        if (ll && !ll_ok(kPhRS, s, b)) return;
       }
       float vmax;
       if (s == 0) stamp(P, wid, lr, 15);  // (p = 2: slot 15 is free) pass A done
@@ -598,8 +612,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const FV<E>& acc) {
                         emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
                       });
-        if (!last) warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
-        else publish_last(c, q.s);
+        if (!last) {
+          if (ll) ll_hdr_put(ll_fwd, c, b, B.len, q.s);
+          else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
+        } else {
+          publish_last(c, q.s);
+        }
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
@@ -621,13 +639,22 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       for (int b = 0; b < p && ok; ++b) {
         const Blk B = get_blk(P, b);
         if (B.nch == 0) continue;
-        const uint64_t v = spin_flag(flag_ptr(R.inbox, P.L, ag_slot(p, b), 0), P, R, ctl, err, kPhAG,
-                                     (r - b + p) % p, b);
-        ok = v != 0;
-        vmax = fmaxf(vmax, __fmul_rn(127.f, __uint_as_float((uint32_t)v)));
+        uint32_t sb = 0;
+        if (ll) {  // the block scale sits in the LL header line of the allgather slot
+          uint4 h;
+          ok = ll_get(ll_ptr(R.inbox, P.L, ag_slot(p, b)), h, give_up);
+          sb = h.w;
+        } else {
+          const uint64_t v = spin_flag(flag_ptr(R.inbox, P.L, ag_slot(p, b), 0), P, R, ctl, err, kPhAG,
+                                       (r - b + p) % p, b);
+          ok = v != 0;
+          sb = (uint32_t)v;
+        }
+        if (ok) vmax = fmaxf(vmax, __fmul_rn(127.f, __uint_as_float(sb)));
       }
     }
     __syncwarp();
+    if (ll && !ll_ok(kPhAG, 0, -1)) return;
     if (!__shfl_sync(0xffffffffu, ok, 0)) return;
     qs = q8_make(q8_scale(__shfl_sync(0xffffffffu, vmax, 0)));
     if (wid == 0 && lane_id() == 0) *R.slot_scale = qs.s;
@@ -648,7 +675,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       float sin = 0.f;
       stamp2(P, wid, lr, 9, first && k == 1);
       if (ll) {
-        if (!ll_hdr_get(ll_in, c, kPhAG, step, b, B.len)) return;
+        if (!ll_hdr_get(ll_in, c, kPhAG, step, b, B.len, sin)) return;
       } else if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) {
         return;
       }
@@ -709,7 +736,8 @@ void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError
                    : P.codec == kTrunc16
                        ? (P.ll ? (const void*)ring_allreduce_kernel<kTrunc16, true>
                                : (const void*)ring_allreduce_kernel<kTrunc16, false>)
-                       : (const void*)ring_allreduce_kernel<kQuant8, false>;
+                       : (P.ll ? (const void*)ring_allreduce_kernel<kQuant8, true>
+                               : (const void*)ring_allreduce_kernel<kQuant8, false>);
   // Emulated rings (nlocal > 1) need every CTA co-resident: cooperative
   // launch. A single rank per GPU only needs its G <= #SM CTAs to become
   // resident eventually (no CTA waits on a CTA of its own launch except the
@@ -730,11 +758,12 @@ int ring_warps_per_cta() { return kWarps; }
 
 int ring_max_ctas_per_sm() {
   int m = 1 << 30;
-  const void* fns[5] = {(const void*)ring_allreduce_kernel<kNone, false>,
+  const void* fns[6] = {(const void*)ring_allreduce_kernel<kNone, false>,
                         (const void*)ring_allreduce_kernel<kTrunc16, false>,
                         (const void*)ring_allreduce_kernel<kQuant8, false>,
                         (const void*)ring_allreduce_kernel<kNone, true>,
-                        (const void*)ring_allreduce_kernel<kTrunc16, true>};
+                        (const void*)ring_allreduce_kernel<kTrunc16, true>,
+                        (const void*)ring_allreduce_kernel<kQuant8, true>};
   for (const void* f : fns) {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, kRingThreads, 0);

@@ -174,11 +174,12 @@ def test_p2p_timeout_produces_diagnostic(P):
 
 
 @multigpu
-def test_p2p_ring_in_cuda_graph_replays_bit_exact(P):
+@pytest.mark.parametrize("n", [300_007, 50_001])  # flag protocol / LL protocol (none, trunc16)
+def test_p2p_ring_in_cuda_graph_replays_bit_exact(P, n):
     """The call sequence number lives on the device, so one captured launch
     can be replayed as many calls (what graph-captured training steps need)."""
     from paper_1811_03619_b200.collective import allreduce_into
-    p, n = 2, 300_007
+    p = 2
     g = np.random.default_rng(5)
     ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
     want = {c: OR.ring_allreduce_all(ins, int(c)).outputs[0] for c in P.Codec}
