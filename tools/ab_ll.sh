@@ -1,8 +1,8 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-for np in 2 4; do
+for np in ${NPS:-2 4}; do
   for L in variants/lib_ll*.so; do
     echo "== p=$np ${L##*/}"
-    PIPESGD_LIB=$PWD/$L timeout 300 torchrun --nproc-per-node $np --master-addr 127.0.0.1 --master-port 29512 tools/ring_sweep.py --sizes ${SIZES:-1024,16384,32768,65536,131072,262144,524288,1048576} --codecs none,trunc16 --iters 20 --check 2>&1 | grep '^{'
+    PIPESGD_LIB=$PWD/$L timeout 300 torchrun --nproc-per-node $np --master-addr 127.0.0.1 --master-port 29512 tools/ring_sweep.py --sizes ${SIZES:-1024,65536,262144,1048576} --codecs ${CODECS:-none,trunc16} --iters 20 --check 2>&1 | grep '^{'
   done
 done
