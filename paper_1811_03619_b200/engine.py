@@ -27,6 +27,7 @@ stream waiting for the ring every iteration (engine.py:340-375).
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -192,7 +193,9 @@ class RankEngine:
         self.dev = fm.params.device
         self.n = fm.num_params
         self.cs = torch.cuda.Stream(self.dev)
-        self.ms = torch.cuda.Stream(self.dev)
+        # comm stream priority (PIPESGD_COMM_PRIORITY, lower = higher; 0 = same
+        # as compute): its CTAs are scheduled ahead of compute CTAs as SMs free up
+        self.ms = torch.cuda.Stream(self.dev, priority=int(os.environ.get("PIPESGD_COMM_PRIORITY", "0")))
         self.tracing = trace
         self.events: list = []  # (iteration, stage, ev0, ev1, consumed)
         K = max(config.depth, 1)
