@@ -93,10 +93,10 @@ def test_fused_variants_emulated(P, p):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("n", [4_710_538, 150_001])  # flag protocol / LL protocol
 @pytest.mark.parametrize("codec", [0, 1, 2])
-def test_fused_variants_p2p(P, codec):
+def test_fused_variants_p2p(P, codec, n):
     p = 4 if NGPU >= 4 else 2
-    n = 4_710_538
     tr = P.GpuTransport(p, timeout_s=60.0, max_elems=n)
     devs = [torch.device("cuda", r) for r in range(p)]
     try:
