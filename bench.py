@@ -536,6 +536,30 @@ def our_arm(args, ws, rank, local):
     if N > 1 and not args.no_allreduce_sweep:
         allreduce = ring_vs_nccl(ep, args.codec, N, dev, [1024, n, 1 << 26], ctas_list=(0, FULL_CTAS))
 
+    # Eq. 5 symbols calibrated on this box in this run: rank 0
+    # drives GPUs 0 and 1 with the flag ping-pong and peer-push kernels while
+    # the other ranks wait
+    calib = None
+    if N > 1 and not args.no_allreduce_sweep:
+        # GPU 1 must be idle while rank 0 runs the ping-pong on it (kernels of
+        # two processes are time-sliced, not concurrent): the other ranks wait
+        # on the TCP store, not in an NCCL barrier kernel
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        store = dist.distributed_c10d._get_default_store()
+        if rank == 0:
+            from paper_1811_03619_b200.timing import calibrate_nvlink
+            try:
+                calib = calibrate_nvlink(devices=(0, 1), nbytes=256 << 20, ctas=148, iters=4000)
+            except RuntimeError as e:
+                print(f"Eq. 5 calibration skipped: {e}", file=sys.stderr)
+            finally:
+                store.set("pipesgd_eq5_calibration", "done")
+        else:
+            store.wait(["pipesgd_eq5_calibration"])
+        torch.cuda.synchronize(dev)
+
     line = None
     if rank == 0:
         h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
@@ -567,7 +591,7 @@ def our_arm(args, ws, rank, local):
                 "codec_none_frac": none_gbs / NVLINK_PEAK_GBS if none_gbs else None,
                 "note": "the same ring kernel alone on a 256 MiB fp32 bucket with every SM (standalone "
                         "allreduce configuration); the engine runs it on %d CTAs beside the CNN" % args.ctas}
-        line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms)
+        line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms, calib)
     return line
 
 
@@ -640,6 +664,8 @@ def isolated_kernels(eng, codec, N, dev, reps=20):
         out["compress"] = timeit(lambda: roundtrip_async(g, codec, loc, st, s.cuda_stream))
     if N == 1 or not eng.fused:
         out["recompress"] = timeit(lambda: encode_async(g, codec, slot.payload, st, s.cuda_stream))
+    if N > 1:  # Eq. 5's gamma: the codec's D(C(.)) pass over the step's gradient on one GPU
+        out["roundtrip"] = timeit(lambda: roundtrip_async(g, codec, loc, st, s.cuda_stream))
     if N > 1:
         if eng.fused:  # the comm stream's single kernel: D(C(g)) -> ring -> C(sum) into the slot
             out["ring"] = timeit(lambda: allreduce_into(g, eng.summed, eng.ep, codec, 0, s, precompress=True,
@@ -701,7 +727,7 @@ def ring_vs_nccl(ep, codec, N, dev, sizes, ctas_list=(0,)):
     return out
 
 
-def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms):
+def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None):
     """The paper's timing model (timing.py:97-132, harness.py:667-720) with
     GPU-measured symbols. Ring: Eq. 5 T = 2(p-1)a + 2(p-1)/p n b (+ n g + S
     folded into a: the fused kernel overlaps its reduction with the transfer),
@@ -735,6 +761,25 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms):
                     "ring_isolated_barrier_aligned_ms": iso.get("ring"),
                     "eq5_over_measured": pred / meas if meas else None,
                     "within_25pct": bool(meas and abs(pred / meas - 1) <= 0.25)})
+        if calib:
+            # SURVEY 8(d) form: T = 2(p-1) a + 2(p-1)/p nb b + (p-1)/p nb g + S with
+            # a = one-way flag latency (gp_calib_pingpong), b = bidirectional peer
+            # push (gp_calib_p2p_copy), g = the codec's D(C(.)) pass per payload
+            # byte on one GPU, S = the 4 KiB ring's time beyond its 2(p-1) flag hops
+            a, b = max(0.0, calib["alpha_s"]), calib["beta_s_per_byte"]
+            nb = n * w
+            g = (iso["roundtrip"] * 1e-3 / nb) if iso.get("roundtrip") else 0.0
+            S = max(0.0, t_small - 2 * (N - 1) * a)
+            terms = {"latency": 2 * (N - 1) * a, "bandwidth": 2 * (N - 1) / N * nb * b,
+                     "reduction": (N - 1) / N * nb * g, "fixed": S}
+            pc = sum(terms.values())
+            out["eq5_calibrated"] = {
+                "alpha_us": a * 1e6, "beta_push_gbs": calib["push_gbs"], "gamma_gbs": 1 / g / 1e9 if g else None,
+                "S_us": S * 1e6, "terms_us": {k: v * 1e6 for k, v in terms.items()},
+                "pred_ms": pc * 1e3, "ring_measured_ms": meas * 1e3, "pred_over_measured": pc / meas if meas else None,
+                "note": "the paper's model assumes one pipelined transfer per hop; the fused ring overlaps the "
+                        "reduction with the transfer (gamma term pessimistic) but pays a fence-bounded phase "
+                        "ramp at this size (profiles/r01_ring_latency)"}
     return out
 
 

@@ -211,6 +211,9 @@ def calibrate_nvlink(devices=(0, 1), nbytes: int = 1 << 30, ctas: int = 148, ite
                       ns[i].data_ptr(), st[i].cuda_stream)
     for s in st:
         s.synchronize()
-    alpha = ns[0].item() / iters / 2 / 1e9
+    t = ns[0].item()
     tr.close()
+    if t < 0:  # the kernel's timeout sentinel (~0): the partner never answered
+        raise RuntimeError("flag ping-pong timed out (is the peer GPU busy with another process?)")
+    alpha = t / iters / 2 / 1e9
     return {"alpha_s": alpha, "beta_s_per_byte": beta, "push_gbs": 1 / beta / 1e9}
