@@ -349,33 +349,35 @@ def our_arm(args, ws, rank, local):
     if args.channels_last and len(in_shape) == 3:
         x_host = x_host.contiguous(memory_format=torch.channels_last).pin_memory()
     x_dev, y_dev = x_host.to(dev), y_host.to(dev)
-    mode = {"e2e": False}
-    x_buf = torch.empty_like(x_dev)  # keeps x_dev's memory format
-    y_buf = torch.empty_like(y_dev)
-
+    mode = {"e2e": False, "end": 0}
     use_graphs = bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused)
+    # Inputs: one buffer per pipeline parity. In e2e mode step t's batch is
+    # copied from pinned host memory into buffer t % NB on a copy stream while
+    # step t-1 computes (every step's copy stays inside the timed region);
+    # resident mode leaves the buffers alone.
+    bufs = {}
+    copy_stream = torch.cuda.Stream(dev)
 
-    def batch_fn(r, t):
-        if mode["e2e"]:  # host->device copy of this step's batch from pinned memory
-            x_buf.copy_(x_host, non_blocking=True)
-            y_buf.copy_(y_host, non_blocking=True)
-            return x_buf, y_buf
-        return x_dev, y_dev
-
-    if use_graphs:
-        # graphs read fixed input tensors: resident mode leaves them alone, e2e
-        # mode refills them in place from pinned host memory every step
-        x_buf.copy_(x_dev)
-        y_buf.copy_(y_dev)
-
-        def batch_fn(r, t):  # noqa: F811
-            if mode["e2e"]:
-                x_buf.copy_(x_host, non_blocking=True)
-                y_buf.copy_(y_host, non_blocking=True)
-            return x_buf, y_buf
+    def batch_fn(r, tt):
+        b = tt % bufs["nb"]
+        if mode["e2e"]:
+            eng.cs.wait_event(bufs["copied"][b])
+        return bufs["x"][b], bufs["y"][b]
 
     eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True, fused=bool(args.fused))
     loss_host = torch.zeros(total_steps + 2, dtype=torch.float32).pin_memory()
+    nb = eng.K if eng.K >= 2 else 1  # buffer index == graph parity
+    bufs.update(nb=nb, x=[x_dev.clone() for _ in range(nb)], y=[y_dev.clone() for _ in range(nb)],
+                copied=[torch.cuda.Event() for _ in range(nb)], free=[torch.cuda.Event() for _ in range(nb)])
+
+    def prefetch(tt):
+        """H2D copy of step tt's batch into its buffer, once the step that read it last is done."""
+        b = tt % nb
+        copy_stream.wait_event(bufs["free"][b])
+        with torch.cuda.stream(copy_stream):
+            bufs["x"][b].copy_(x_host, non_blocking=True)
+            bufs["y"][b].copy_(y_host, non_blocking=True)
+        bufs["copied"][b].record(copy_stream)
 
     def barrier():
         if N > 1:
@@ -389,6 +391,10 @@ def our_arm(args, ws, rank, local):
         start = torch.cuda.Event(enable_timing=True)
         start.record(eng.cs)
         eng.ms.wait_stream(eng.cs)
+        mode["end"] = t0 + steps
+        if e2e:
+            copy_stream.wait_stream(eng.cs)
+            prefetch(t0)
         for t in range(t0, t0 + steps):
             step(t)
             if e2e:  # device->host read of the step's loss (async into pinned memory)
@@ -404,7 +410,19 @@ def our_arm(args, ws, rank, local):
         return max_over_ranks(ms, dev), list(eng.events)
 
     pipe = args.mode == "pipe_sgd"
-    step = eng.step if pipe else (eng.ps_step if args.mode == "ps_sync" else eng.step_sync)
+    inner = eng.step if pipe else (eng.ps_step if args.mode == "ps_sync" else eng.step_sync)
+
+    def step(tt):
+        if use_graphs and "graphs" in bufs:
+            if mode["e2e"]:
+                eng.cs.wait_event(bufs["copied"][tt % nb])
+            eng.step_graph(tt)
+        else:
+            inner(tt)  # batch_fn waits for the copy
+        bufs["free"][tt % nb].record(eng.cs)
+        if mode["e2e"] and tt + 1 < mode["end"]:
+            prefetch(tt + 1)
+
     with torch.cuda.device(dev), torch.cuda.stream(eng.cs):
         if pipe:
             eng.prime(1)
@@ -413,12 +431,9 @@ def our_arm(args, ws, rank, local):
             step(t)
             t += 1
         if use_graphs:
-            eng.capture_graphs((x_buf, y_buf))
-
-            def step(tt):  # noqa: F811
-                if mode["e2e"]:
-                    batch_fn(rank, tt)
-                eng.step_graph(tt)
+            # compute graph i reads input buffer i (per-parity buffers)
+            eng.capture_graphs([(bufs["x"][i % nb], bufs["y"][i % nb]) for i in range(eng.K)])
+            bufs["graphs"] = True
 
             for _ in range(max(2, eng.K)):
                 step(t)
@@ -570,8 +585,9 @@ def our_arm(args, ws, rank, local):
                 "config": workload_config(args, n, N),
                 "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d * N,
                         "d2h_bytes_per_step": 4 * N,
-                        "how": "same engine; every step copies the rank's batch from pinned host memory and "
-                               "reads the loss back"},
+                        "how": "same engine; every step copies the rank's batch from pinned host memory (on a "
+                               "copy stream into a per-parity buffer, overlapping the previous step's compute) "
+                               "and reads the loss back"},
                 "gpu_launches": per_iter_launches * args.steps,
                 "roofline": roof, "kernels": kernels, "clocks": clk.summary(),
                 "samples_per_s": value * args.global_batch}

@@ -419,14 +419,18 @@ class RankEngine:
             raise ConfigError("graph mode needs fused pipe_sgd or d_sync with a constant learning rate and a model")
         if type(self.ep).__name__ == "EmulatedEndpoint":
             raise ConfigError("graph mode needs one GPU per rank (the emulated ring rendezvouses on the host)")
-        x, y = batch
+        # one (x, y) for every parity, or a list of K (x, y): compute graph i
+        # reads batch i (double-buffered inputs prefetched on a copy stream)
+        batches = list(batch) if isinstance(batch, list) else [batch] * self.K
+        if len(batches) != self.K:
+            raise ConfigError(f"need {self.K} per-parity batches, got {len(batches)}")
         lr = float(np.float32(cfg.learning_rate))
         self.static_loss = [torch.zeros((), dtype=torch.float32, device=self.dev) for _ in range(self.K)]
         self.g_update, self.g_compute, self.g_comm = [], [], []
         self.ev_agg = [torch.cuda.Event() for _ in range(self.K)]
         torch.cuda.synchronize(self.dev)
         if cfg.mode == MODE_D_SYNC:
-            self._capture_sync_graphs(x, y, lr)
+            self._capture_sync_graphs(batches, lr)
             return
         for i in range(self.K):
             slot = self.slots[i]
@@ -438,7 +442,7 @@ class RankEngine:
             gc = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
                 self.fm.use_grad_buffer(i)
-                self.static_loss[i].copy_(self.fm.loss_and_grad(x, y))
+                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
             gm = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gm, stream=self.ms, capture_error_mode="thread_local"):
                 g = self.fm.grad_bufs[i]
@@ -451,7 +455,7 @@ class RankEngine:
             self.g_comm.append(gm)
         self.graph_ready_tag = {}
 
-    def _capture_sync_graphs(self, x, y, lr) -> None:
+    def _capture_sync_graphs(self, batches, lr) -> None:
         K, codec = self.K, self.cfg.codec
         for i in range(K):
             pend = self.sync_slots[(i - 1) % K]  # holds the sum of t-1 when t % K == i
@@ -462,7 +466,7 @@ class RankEngine:
             gc = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
                 self.fm.use_grad_buffer(i)
-                self.static_loss[i].copy_(self.fm.loss_and_grad(x, y))
+                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
             gm = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gm, stream=self.cs, capture_error_mode="thread_local"):
                 g = self.fm.grad_bufs[i]
