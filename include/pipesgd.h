@@ -90,7 +90,7 @@ int gp_comm_ipc_handle(gp_comm* comm, void* handle_out /* 64 bytes */);
 int gp_comm_connect_ipc(gp_comm* comm, const void* handles /* world x 64 bytes, rank order */);
 int gp_comm_connect_local(gp_comm* const* comms, int world);
 int gp_comm_set_tuning(gp_comm* comm, int ctas_per_rank, double timeout_s);
-/* Optional ring timeline for profiling: device buffer of nlocal x ctas x 16 warps
+/* Optional ring timeline for profiling: device buffer of nlocal x ctas x 4 warps
  * x 20 u64 %globaltimer stamps (see csrc/ring.cuh kTraceSlots); NULL disables. */
 int gp_comm_set_trace(gp_comm* comm, void* device_buffer);
 int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, emulated] */);

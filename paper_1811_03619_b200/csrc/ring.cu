@@ -231,7 +231,7 @@ __device__ __forceinline__ void warp_publish_all(const RingParams& P, const Rank
   }
 }
 
-// quant8: rank-wide barrier over all 16G warps of one rank carrying the
+// quant8: rank-wide barrier over all G x kWarps warps of one rank carrying the
 // block max. Returns false on abort/timeout.
 __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err, int k,
                                  uint32_t mymax, float& vmax, int step) {

@@ -90,14 +90,16 @@ struct RingParams {
   uint64_t timeout_ns;
   uint32_t iteration;
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
-  int p, codec, G;             // world size, codec tag, CTAs per rank (16 warp workers each)
+  int p, codec, G;             // world size, codec tag, CTAs per rank (kRingWarps warp workers each)
   int pre;                     // x is the raw gradient: apply the local D(C(.)) on load
   int ll;                      // this call uses the LL protocol (see ll_payload_limit)
   unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
 
 constexpr int kTraceSlots = 20;  // [0] start, [1] step-0 send done, [2+2s] step s first chunk
-                                 // in, [3+2s] step s done, [18] allgather first in, [19] end
+                                 // in, [3+2s] step s done, [15-17] quant8 pass/barrier stamps,
+                                 // [18] allgather first in, [19] end; at p = 2 slots 4-9 hold
+                                 // the first chunk's fold/send/allgather sub-stamps
 
 __host__ __device__ inline int rs_slot(int s) { return s; }
 __host__ __device__ inline int ag_slot(int p, int b) { return p - 1 + b; }
