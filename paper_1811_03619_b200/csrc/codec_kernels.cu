@@ -11,6 +11,7 @@
 // step with 16/32-byte vector accesses, grid = a multiple of the SM count,
 // grid-stride loops. quant8 needs max|x| before any code can be written,
 // so it is two launches: absmax (atomicMax of float bits) then encode.
+#include <cstdlib>
 #include <string>
 
 #include "../../include/pipesgd.h"
@@ -48,9 +49,13 @@ uint32_t grid_for(uint64_t n) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
+  static const uint64_t per_sm = [] {
+    const char* e = std::getenv("PIPESGD_CU_GRID_PER_SM");
+    return (uint64_t)(e ? std::max(1, std::atoi(e)) : 8);
+  }();
   const uint64_t per_block = (uint64_t)kT * std::max(kElems, 16);
   const uint64_t want = (n + per_block - 1) / per_block;
-  const uint64_t cap = (uint64_t)sms * 8;
+  const uint64_t cap = (uint64_t)sms * per_sm;
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
 
