@@ -277,3 +277,31 @@ def test_p2p_ring_across_call_sequence_wrap(P):
                         assert_bits_equal(y.cpu().numpy(), want, f"k={k} n={n} {codec.name} rank {r}")
     finally:
         tr.close()
+
+
+@pytest.mark.parametrize("p", [3] + ([2] if NGPU >= 2 else []))
+def test_empty_vector_ring_matches_reference(P, p):
+    """n = 0 (the reference returns empty arrays and still counts 2(p-1)
+    messages of 0 payload / 20 frame bytes each; checked against the oracle,
+    which reproduces the reference's stats)."""
+    emulated = p == 3
+    tr = P.EmulatedTransport(p, timeout_s=30.0, max_elems=64) if emulated else P.GpuTransport(p, timeout_s=30.0,
+                                                                                             max_elems=64)
+    try:
+        ins = [np.zeros(0, np.float32) for _ in range(p)]
+        for codec in P.Codec:
+            want = OR.ring_allreduce_all(ins, int(codec))
+
+            def op(r, ep):
+                ep.reset_stats()
+                y = P.ring_allreduce(ins[r], r, p, ep, codec, iteration=2)
+                s = ep.stats
+                return y, (s.messages, s.payload_bytes, s.frame_bytes)
+
+            res = run_ranks(tr, op)
+            for r, (y, st) in enumerate(res):
+                assert y.shape == (0,) and y.dtype == np.float32
+                w = want.stats[r]
+                assert st == (w.messages, w.payload_bytes, w.frame_bytes), (codec, r, st)
+    finally:
+        tr.close()
