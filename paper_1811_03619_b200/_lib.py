@@ -11,7 +11,7 @@ import ctypes
 import os
 import threading
 
-from .errors import NativeLibraryError
+from .errors import ConfigError, NativeLibraryError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PIPESGD_LIB") or os.path.join(HERE, "libpipesgd.so")
@@ -106,9 +106,13 @@ def load() -> ctypes.CDLL:
 
 
 def check(rc: int, what: str) -> None:
+    """GP_ERR_ARG / GP_ERR_STATE (a caller error: size over capacity, bad
+    codec, misalignment, unconnected communicator) raise the reference's
+    ConfigError; CUDA and platform failures raise NativeLibraryError."""
     if rc != GP_OK:
         msg = load().gp_last_error_string().decode(errors="replace")
-        raise NativeLibraryError(f"{what} failed (code {rc}): {msg}")
+        cls = ConfigError if rc in (1, 3) else NativeLibraryError  # GP_ERR_ARG, GP_ERR_STATE
+        raise cls(f"{what} failed (code {rc}): {msg}")
 
 
 def call(name: str, *args) -> None:

@@ -305,3 +305,15 @@ def test_empty_vector_ring_matches_reference(P, p):
                 assert st == (w.messages, w.payload_bytes, w.frame_bytes), (codec, r, st)
     finally:
         tr.close()
+
+
+def test_call_over_capacity_is_a_config_error(P):
+    """A vector longer than the communicator was created for is a caller
+    error (ConfigError), reported before any launch."""
+    tr = P.EmulatedTransport(2, timeout_s=10.0, max_elems=1000)
+    try:
+        ins = [np.ones(1001, np.float32) for _ in range(2)]
+        with pytest.raises(P.ConfigError, match="capacity"):
+            run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, 2, ep, P.Codec.NONE))
+    finally:
+        tr.close()
