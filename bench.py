@@ -737,7 +737,12 @@ def ring_vs_nccl(ep, codec, N, dev, sizes, ctas_list=(0,)):
             ms = max_over_ranks(a.elapsed_time(b) / it, dev)
             if name != "nccl":
                 endpoint_wait(ep, n, s)
-            res[key] = {"ms": ms, "busbw_gbs": 2 * (N - 1) / N * 4 * n / (ms * 1e-3) / 1e9}
+            rec = {"ms": ms, "busbw_gbs": 2 * (N - 1) / N * 4 * n / (ms * 1e-3) / 1e9}
+            if name != "nccl":  # wire bytes actually moved, as a fraction of the NVLink peak
+                wb = {"none": 4, "trunc16": 2, "quant8": 1}[name]
+                rec["wire_busbw_gbs"] = 2 * (N - 1) / N * wb * n / (ms * 1e-3) / 1e9
+                rec["nvlink_frac"] = rec["wire_busbw_gbs"] / NVLINK_PEAK_GBS
+            res[key] = rec
         _lib.call("gp_comm_set_tuning", ep._comm, int(base), 0.0)
         out.append(res)
     return out
