@@ -535,7 +535,8 @@ def our_arm(args, ws, rank, local):
                             "(sharing HBM and SMs with the other stream); the same kernel alone, L2 flushed "
                             f"before each launch: {kd.get('isolated_hbm_gbs', 0):.1f} GB/s",
                 "achieved_isolated": kd.get("isolated_hbm_gbs"),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else
+                                "of fallback: B200_PROFILING.md 6.65 TB/s (MEASURED_PEAKS.json absent)"),
                 "same_size_torch_copy_gbs": copy_gbs,
                 "note": "at this vector size (%d fp32) launch/ramp latency bounds every kernel: torch's own "
                         "copy of 8n bytes reaches %.0f GB/s by the same method" % (n, copy_gbs),
