@@ -27,6 +27,9 @@
  *                           aggregate_mean -> models.py:198-204 sgd_update
  *   gp_calib_p2p_copy       harness.py:552-557 beta probe (flood), on NVLink
  *   gp_calib_pingpong       harness.py:547-550 alpha probe (1-byte ping), on NVLink
+ *   gp_comm_set_tuning / _set_trace / _info / _set_call_counter: no reference
+ *                           counterpart (CTA budget + timeout, timeline stamps,
+ *                           introspection, 32-bit sequence-wrap test hook)
  *
  * Return value: GP_OK (0) or a GP_ERR_* code; gp_last_error_string() gives
  * the calling thread's last message. Failures detected on the device
