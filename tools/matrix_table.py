@@ -5,6 +5,7 @@ import os
 import sys
 
 ROWS = [("c1_pipe", "C1 MNIST MLP, none", "Pipe-SGD width 2 (graphs)"),
+        ("c1_sync", "C1 MNIST MLP, none", "D-Sync width 1 (graphs)"),
         ("c2_pipe", "C2 CIFAR CNN, trunc16", "Pipe-SGD width 2 (graphs)"),
         ("c2_pipe_eager", "C2 CIFAR CNN, trunc16", "Pipe-SGD width 2 (eager)"),
         ("c2_sync", "C2 CIFAR CNN, trunc16", "D-Sync width 1 (graphs)"),
@@ -42,7 +43,7 @@ def main(d):
         print(f"| {cfg} | {scheme} | " + " | ".join(cells) + " |")
     print()
     print("Speed-ups at N=4:")
-    for m in ("c2", "c3", "c4"):
+    for m in ("c1", "c2", "c3", "c4"):
         for a, b in (("pipe", "sync"), ("pipe_eager", "sync_eager"), ("pipe", "ps"), ("pipe_eager", "ps")):
             x, y = vals.get((f"{m}_{a}", 4)), vals.get((f"{m}_{b}", 4))
             if x and y:

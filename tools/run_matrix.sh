@@ -20,6 +20,7 @@ run() {  # name ngpu args...
 Q="--no-cpu-baseline --no-allreduce-sweep"
 for n in 1 2 4; do
   run c1_pipe_n$n $n --model c1 --codec none --global-batch 100 --steps 300 --warmup 30 $Q
+  run c1_sync_n$n $n --model c1 --codec none --mode d_sync --global-batch 100 --steps 300 --warmup 30 $Q
   run c2_pipe_n$n $n --steps 100 --warmup 10 $Q
   run c2_pipe_eager_n$n $n --graphs 0 --steps 100 --warmup 10 $Q
   run c2_sync_n$n $n --mode d_sync --steps 100 --warmup 10 $Q
