@@ -1,5 +1,4 @@
 """Markdown table of a run_matrix.sh output directory (one bench JSON per cell)."""
-import glob
 import json
 import os
 import sys

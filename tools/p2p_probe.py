@@ -1,7 +1,6 @@
 """NVLink ceilings on this box (2 GPUs, one process): kernel push/pull copy
 rates vs CTA count, uni- and bidirectional, copy-engine memcpy, flag
 ping-pong latency. Output: JSON lines."""
-import ctypes
 import json
 import os
 import sys

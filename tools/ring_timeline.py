@@ -7,7 +7,6 @@ the earliest kernel start on that GPU (us), plus the CUDA-event time of the
 same call, so launch overhead / flag latency / streaming time separate.
 """
 import argparse
-import ctypes
 import json
 import os
 import sys
