@@ -522,8 +522,11 @@ def our_arm(args, ws, rank, local):
                 "algorithmic_bytes_per_launch": wire}
     else:
         copy_gbs = 8 * n / (iso["copy_4n"] * 1e-3) / 1e9
+        # dominant = the kernel with the longest duration of its own (isolated):
+        # at N = 1 the update and the encode overlap each other inside the
+        # step, so their in-step times swap order from run to run
         dom = max([k for k in ("update", "compress", "recompress") if k in kernels and avg.get(k)],
-                  key=lambda k: avg[k])
+                  key=lambda k: iso.get(k) or avg[k])
         name = {"update": "consume_update_kernel", "compress": "roundtrip_kernel",
                 "recompress": "encode_kernel"}[dom]
         kd = kernels[dom]

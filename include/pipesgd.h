@@ -23,7 +23,7 @@
  *                           compression.py:108-109 CodecError (non-finite)
  *   gp_encode / gp_decode   compression.py:103-136 compress, :141-151 decompress
  *   gp_roundtrip            engine.py:333 + :355/:400 decompress(compress(grad))
- *   gp_consume_update       engine.py:420-426 decompress -> engine.py:123-129
+ *   gp_consume_update(_dev) engine.py:420-426 decompress -> engine.py:123-129
  *                           aggregate_mean -> models.py:198-204 sgd_update
  *   gp_calib_p2p_copy       harness.py:552-557 beta probe (flood), on NVLink
  *   gp_calib_pingpong       harness.py:547-550 alpha probe (1-byte ping), on NVLink
@@ -146,6 +146,11 @@ int gp_roundtrip(int codec, const float* in, float* out, uint64_t n, gp_codec_st
                  void* stream);
 int gp_consume_update(float* params, int codec, const void* slot, const float* slot_scale,
                       uint64_t n, float lr, int world, void* stream);
+/* Same, with the learning rate read from device memory (one fp32): a CUDA
+ * graph captures this call once and each replay uses the rate the host wrote
+ * before it (models.py / engine.py:287-292 learning-rate decay under replay). */
+int gp_consume_update_dev(float* params, int codec, const void* slot, const float* slot_scale,
+                          uint64_t n, const float* lr, int world, void* stream);
 
 /* ---- calibration (timing-model alpha/beta on NVLink) ------------------- */
 int gp_calib_p2p_copy(void* dst, const void* src, uint64_t bytes, int ctas, int pull, void* stream);

@@ -29,7 +29,7 @@ EXPORTS = (
     "gp_allreduce", "gp_allreduce_ex", "gp_allreduce_emulated", "gp_allreduce_emulated_ex",
     "gp_gather_sum", "gp_broadcast", "gp_gather_sum_emulated", "gp_broadcast_emulated",
     "gp_comm_poll_error", "gp_get_stats",
-    "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update",
+    "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update", "gp_consume_update_dev",
     "gp_calib_p2p_copy", "gp_calib_p2p_copy_ex", "gp_calib_pingpong", "gp_last_error_string", "gp_version",
 )
 
@@ -74,6 +74,7 @@ _SIGS = {
     "gp_decode": (_i, [_i, _vp, _vp, _u64, _vp, _vp]),
     "gp_roundtrip": (_i, [_i, _vp, _vp, _u64, _vp, _vp]),
     "gp_consume_update": (_i, [_vp, _i, _vp, _vp, _u64, _f, _i, _vp]),
+    "gp_consume_update_dev": (_i, [_vp, _i, _vp, _vp, _u64, _vp, _i, _vp]),
     "gp_calib_p2p_copy": (_i, [_vp, _vp, _u64, _i, _i, _vp]),
     "gp_calib_p2p_copy_ex": (_i, [_vp, _vp, _u64, _i, _i, _u64, _vp, _vp, _vp]),
     "gp_calib_pingpong": (_i, [_vp, _vp, _i, _i, _u64, _vp, _vp]),

@@ -146,9 +146,10 @@ __global__ void __launch_bounds__(kT) roundtrip_kernel(const float* __restrict__
 
 template <int C>
 __global__ void __launch_bounds__(kT, PIPESGD_CU_MINB) consume_update_kernel(float* w, const uint8_t* slot, const float* scale,
-                                                            uint64_t n, float lr, int p) {
+                                                            uint64_t n, float lr_val, const float* lr_dev, int p) {
   constexpr int E = CodecT<C>::E;
   const float s = (C == kQuant8) ? *scale : 0.f;
+  const float lr = lr_dev ? __ldg(lr_dev) : lr_val;  // device-resident rate: graph replays with decay
   const float fp = (float)p;
   struct WG {
     FV<E> w;
@@ -245,8 +246,8 @@ int gp_roundtrip(int codec, const float* in, float* out, uint64_t n, gp_codec_st
   return check_launch("roundtrip kernel");
 }
 
-int gp_consume_update(float* w, int codec, const void* slot, const float* scale, uint64_t n, float lr,
-                      int world, void* stream) {
+static int consume_update(float* w, int codec, const void* slot, const float* scale, uint64_t n, float lr,
+                          const float* lr_dev, int world, void* stream) {
   if (codec < 0 || codec > 2) return cfail(GP_ERR_ARG, "unknown codec");
   if (world < 1) return cfail(GP_ERR_ARG, "worker count must be >= 1");
   if (n && (!w || !slot)) return cfail(GP_ERR_ARG, "null buffer");
@@ -256,10 +257,21 @@ int gp_consume_update(float* w, int codec, const void* slot, const float* scale,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t g = grid_for(n);
   auto* pl = static_cast<const uint8_t*>(slot);
-  if (codec == kQuant8) consume_update_kernel<kQuant8><<<g, kT, 0, s>>>(w, pl, scale, n, lr, world);
-  else if (codec == kTrunc16) consume_update_kernel<kTrunc16><<<g, kT, 0, s>>>(w, pl, scale, n, lr, world);
-  else consume_update_kernel<kNone><<<g, kT, 0, s>>>(w, pl, scale, n, lr, world);
+  if (codec == kQuant8) consume_update_kernel<kQuant8><<<g, kT, 0, s>>>(w, pl, scale, n, lr, lr_dev, world);
+  else if (codec == kTrunc16) consume_update_kernel<kTrunc16><<<g, kT, 0, s>>>(w, pl, scale, n, lr, lr_dev, world);
+  else consume_update_kernel<kNone><<<g, kT, 0, s>>>(w, pl, scale, n, lr, lr_dev, world);
   return check_launch("consume_update kernel");
+}
+
+int gp_consume_update(float* w, int codec, const void* slot, const float* scale, uint64_t n, float lr,
+                      int world, void* stream) {
+  return consume_update(w, codec, slot, scale, n, lr, nullptr, world, stream);
+}
+
+int gp_consume_update_dev(float* w, int codec, const void* slot, const float* scale, uint64_t n,
+                          const float* lr, int world, void* stream) {
+  if (n && !lr) return cfail(GP_ERR_ARG, "null learning-rate pointer");
+  return consume_update(w, codec, slot, scale, n, 0.f, lr, world, stream);
 }
 
 }  // extern "C"

@@ -411,12 +411,12 @@ class RankEngine:
         Replays are linked by events between the streams, so iteration t's
         ring still overlaps iteration t+1's compute. The ring kernel reads its
         call sequence number on the device, so every replay is a new call.
-        Requirements: pipe mode, fused path, real GPU transport, constant
-        learning rate, static batch tensors (refilled in place by the caller)."""
+        Requirements: pipe or d_sync mode, fused path, real GPU transport,
+        static batch tensors (refilled in place by the caller). Learning-rate
+        decay works: the update graphs read the rate from device memory."""
         cfg = self.cfg
-        if (not self.fused or cfg.mode not in (MODE_PIPE_SGD, MODE_D_SYNC) or cfg.lr_decay_every > 0
-                or self.grad_fn is not None):
-            raise ConfigError("graph mode needs fused pipe_sgd or d_sync with a constant learning rate and a model")
+        if not self.fused or cfg.mode not in (MODE_PIPE_SGD, MODE_D_SYNC) or self.grad_fn is not None:
+            raise ConfigError("graph mode needs fused pipe_sgd or d_sync and a model")
         if type(self.ep).__name__ == "EmulatedEndpoint":
             raise ConfigError("graph mode needs one GPU per rank (the emulated ring rendezvouses on the host)")
         # one (x, y) for every parity, or a list of K (x, y): compute graph i
@@ -424,7 +424,10 @@ class RankEngine:
         batches = list(batch) if isinstance(batch, list) else [batch] * self.K
         if len(batches) != self.K:
             raise ConfigError(f"need {self.K} per-parity batches, got {len(batches)}")
-        lr = float(np.float32(cfg.learning_rate))
+        # the update graphs read the learning rate from device memory, written
+        # before each replay with lr_at(t) (engine.py:287-292 decay)
+        self.lr_dev = torch.full((1,), float(np.float32(cfg.learning_rate)), dtype=torch.float32, device=self.dev)
+        lr = self.lr_dev
         self.static_loss = [torch.zeros((), dtype=torch.float32, device=self.dev) for _ in range(self.K)]
         self.g_update, self.g_compute, self.g_comm = [], [], []
         self.ev_agg = [torch.cuda.Event() for _ in range(self.K)]
@@ -436,8 +439,8 @@ class RankEngine:
             slot = self.slots[i]
             gu = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gu, stream=self.cs, capture_error_mode="thread_local"):
-                _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
-                          slot.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+                _lib.call("gp_consume_update_dev", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
+                          slot.status.scale_view.data_ptr(), self.n, lr.data_ptr(), self.world, self.cs.cuda_stream)
             self.g_update.append(gu)
             gc = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
@@ -461,8 +464,8 @@ class RankEngine:
             pend = self.sync_slots[(i - 1) % K]  # holds the sum of t-1 when t % K == i
             gu = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gu, stream=self.cs, capture_error_mode="thread_local"):
-                _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
-                          pend.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
+                _lib.call("gp_consume_update_dev", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
+                          pend.status.scale_view.data_ptr(), self.n, lr.data_ptr(), self.world, self.cs.cuda_stream)
             gc = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
                 self.fm.use_grad_buffer(i)
@@ -491,6 +494,7 @@ class RankEngine:
         elif self.graph_pending != t - 1:
             raise ConfigError("d_sync graph steps must be consecutive")
         tr = self.tracing
+        self._set_lr(t)
         e0 = self._ev(self.cs) if tr else None
         self.g_update[i].replay()
         e1 = self._ev(self.cs) if tr else None
@@ -519,6 +523,7 @@ class RankEngine:
         else:  # slot i still holds the eager pipeline's tag t-K: wait for it
             self.buffer.take(t - self.K, self.cs)
         tr = self.tracing
+        self._set_lr(t)
         e0 = self._ev(self.cs) if tr else None
         self.g_update[i].replay()
         eu = self._ev(self.cs) if tr else None
@@ -539,11 +544,18 @@ class RankEngine:
         self.graph_ready_tag[i] = t
         self._mark(t)
 
+    def _set_lr(self, t: int) -> None:
+        """Learning rate of update t into the device scalar the update graphs read."""
+        if self.cfg.lr_decay_every > 0:
+            with torch.cuda.stream(self.cs):
+                self.lr_dev.fill_(float(np.float32(self._lr(t))))
+
     def drain_graph(self, t1: int) -> None:
-        lr = float(np.float32(self.cfg.learning_rate))
+        """The last updates eagerly, with the eager engine's rates (drain / drain_sync)."""
         if self.cfg.mode == MODE_D_SYNC:
             if self.graph_pending is not None:
                 pend = self.sync_slots[self.graph_pending % self.K]
+                lr = float(np.float32(self._lr(self.graph_pending + 1)))
                 _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
                           pend.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
                 self.graph_pending = None
@@ -552,6 +564,7 @@ class RankEngine:
             i = tag % self.K
             self.cs.wait_event(self.ev_agg[i])
             slot = self.slots[i]
+            lr = float(np.float32(self._lr(tag + self.K)))
             _lib.call("gp_consume_update", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
                       slot.status.scale_view.data_ptr(), self.n, lr, self.world, self.cs.cuda_stream)
 

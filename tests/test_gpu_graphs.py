@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd"):
+def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0):
     from paper_1811_03619_b200.engine import RankEngine, RunConfig
     from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
     spec = ModelSpec("mlp", (64, 128, 10))
@@ -26,7 +26,8 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd"):
             g = torch.Generator(device="cpu").manual_seed(10 + r)
             x = torch.randn(32, 64, generator=g).to(dev)
             y = torch.randint(0, 10, (32,), generator=g).to(dev)
-            cfg = RunConfig(mode=mode, iterations=T + 2, learning_rate=0.05, codec=codec, batch_size=32)
+            cfg = RunConfig(mode=mode, iterations=T + 2, learning_rate=0.05, codec=codec, batch_size=32, depth=depth,
+                            lr_decay_every=decay, lr_decay_factor=0.5 if decay else 1.0)
             eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False)
             pipe = mode == "pipe_sgd"
             step = eng.step if pipe else eng.step_sync
@@ -67,3 +68,32 @@ def test_graph_replay_matches_eager(P, p, codec, mode):
         np.testing.assert_array_equal(graph[r][1], eager[r][1])
     for r in range(1, p):
         assert_bits_equal(graph[r][0], graph[0][0], "replicas")
+
+
+@pytest.mark.parametrize("codec", [1, 2])
+@pytest.mark.parametrize("p", [1, 2])
+def test_graph_replay_width_3_matches_eager(P, p, codec):
+    if p > NGPU:
+        pytest.skip("needs more GPUs")
+    eager = train(P, p, codec, graphs=False, depth=3)
+    graph = train(P, p, codec, graphs=True, depth=3)
+    for r in range(p):
+        assert_bits_equal(graph[r][0], eager[r][0], f"width 3 p={p} codec={codec} rank {r}")
+        np.testing.assert_array_equal(graph[r][1], eager[r][1])
+
+
+@pytest.mark.parametrize("mode", ["pipe_sgd", "d_sync"])
+@pytest.mark.parametrize("p", [1, 2])
+def test_graph_replay_with_lr_decay_matches_eager(P, p, mode):
+    """engine.py:287-292 decay under replay: the update graphs read the rate
+    from device memory, written before every replay; the drain uses the
+    eager engine's per-tag rates."""
+    if p > NGPU:
+        pytest.skip("needs more GPUs")
+    eager = train(P, p, 1, graphs=False, mode=mode, decay=4)
+    graph = train(P, p, 1, graphs=True, mode=mode, decay=4)
+    for r in range(p):
+        assert_bits_equal(graph[r][0], eager[r][0], f"decay {mode} p={p} rank {r}")
+        np.testing.assert_array_equal(graph[r][1], eager[r][1])
+    const = train(P, p, 1, graphs=True, mode=mode, decay=0)
+    assert not np.array_equal(const[0][0], graph[0][0]), "decay had no effect"
