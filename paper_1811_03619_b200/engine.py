@@ -417,6 +417,10 @@ class RankEngine:
         cfg = self.cfg
         if not self.fused or cfg.mode not in (MODE_PIPE_SGD, MODE_D_SYNC) or self.grad_fn is not None:
             raise ConfigError("graph mode needs fused pipe_sgd or d_sync and a model")
+        if cfg.eval_interval or cfg.snapshot_first:
+            # their host-side snapshots live in the eager step (engine.py run()
+            # keeps them); a replayed step would silently skip them
+            raise ConfigError("graph mode does not take eval_interval / snapshot_first snapshots; run eagerly")
         if type(self.ep).__name__ == "EmulatedEndpoint":
             raise ConfigError("graph mode needs one GPU per rank (the emulated ring rendezvouses on the host)")
         # one (x, y) for every parity, or a list of K (x, y): compute graph i
