@@ -23,6 +23,13 @@ Alg. 1 (update at t consumes the aggregated gradient of t-K; slots for
 tags t_start-K..t_start-1 are zero; K in-flight gradients are drained).
 d_sync is the same machinery with depth 1, no re-compress and the compute
 stream waiting for the ring every iteration (engine.py:340-375).
+
+By default (fused=True) the local pre-compress and the pipe re-compress are
+folded into the single ring kernel of each iteration (gp_allreduce_ex with
+GP_RING_PRECOMPRESS | GP_RING_SLOT_OUT). For the steady state,
+capture_graphs / step_graph replay the iteration as CUDA graphs (update /
+compute / comm per parity, any width, learning-rate decay through a
+device-resident rate), bit-identical to the eager step.
 """
 
 from __future__ import annotations
