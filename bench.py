@@ -371,14 +371,21 @@ def our_arm(args, ws, rank, local):
     bufs.update(nb=nb, x=[x_dev.clone() for _ in range(nb)], y=[y_dev.clone() for _ in range(nb)],
                 copied=[torch.cuda.Event() for _ in range(nb)], free=[torch.cuda.Event() for _ in range(nb)])
 
+    copy_events = []
+
     def prefetch(tt):
         """H2D copy of step tt's batch into its buffer, once the step that read it last is done."""
         b = tt % nb
         copy_stream.wait_event(bufs["free"][b])
+        c0 = torch.cuda.Event(enable_timing=True)
+        c0.record(copy_stream)
         with torch.cuda.stream(copy_stream):
             bufs["x"][b].copy_(x_host, non_blocking=True)
             bufs["y"][b].copy_(y_host, non_blocking=True)
         bufs["copied"][b].record(copy_stream)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c1.record(copy_stream)
+        copy_events.append((c0, c1))
 
     def barrier():
         if N > 1:
@@ -455,7 +462,9 @@ def our_arm(args, ws, rank, local):
         for _ in range(2):
             step(t)
             t += 1
+        copy_events.clear()
         e2e_ms, _ = timed_region(t, args.steps, e2e=True)
+        copy_ms = [a.elapsed_time(b) for a, b in copy_events]
         t += args.steps
         if use_graphs:
             eng.drain_graph(t - 1)
@@ -595,6 +604,7 @@ def our_arm(args, ws, rank, local):
                 "config": workload_config(args, n, N),
                 "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d * N,
                         "d2h_bytes_per_step": 4 * N,
+                        "h2d_copy_ms_avg": float(np.mean(copy_ms)) if copy_ms else None,
                         "how": "same engine; every step copies the rank's batch from pinned host memory (on a "
                                "copy stream into a per-parity buffer, overlapping the previous step's compute) "
                                "and reads its loss back into pinned memory (on a D2H stream after the step)"},
