@@ -61,3 +61,26 @@ def test_partition_blocks_matches_oracle():
     for n in (0, 1, 7, 4099, 61_100_840):
         for p in (1, 2, 3, 4, 8):
             assert partition_blocks(n, p) == ref(n, p)
+
+
+def test_argument_errors_are_reported_without_a_gpu():
+    """Argument validation runs before any CUDA call: GP_ERR_ARG (1), the
+    thread's last-error string, and the Python mapping to ConfigError."""
+    from paper_1811_03619_b200 import _lib
+    from paper_1811_03619_b200.errors import ConfigError
+    lib = _lib.load()
+    buf = (ctypes.c_float * 8)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    cases = [
+        (lambda: lib.gp_encode(7, p, 8, p, p, None), "unknown codec"),
+        (lambda: lib.gp_decode(-1, p, p, 8, p, None), "unknown codec"),
+        (lambda: lib.gp_consume_update(p, 0, p, None, 8, ctypes.c_float(0.1), 0, None), "worker count"),
+        (lambda: lib.gp_consume_update_dev(p, 0, p, None, 8, None, 1, None), "learning-rate pointer"),
+        (lambda: lib.gp_comm_set_call_counter(None, ctypes.c_uint64(0)), "null communicator"),
+        (lambda: lib.gp_comm_set_call_counter(None, ctypes.c_uint64(1 << 33)), "null communicator"),
+    ]
+    for fn, msg in cases:
+        assert fn() == 1
+        assert msg in lib.gp_last_error_string().decode()
+    with pytest.raises(ConfigError, match="unknown codec"):
+        _lib.call("gp_encode", 9, p, 8, p, p, None)
