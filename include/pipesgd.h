@@ -27,9 +27,10 @@
  *                           aggregate_mean -> models.py:198-204 sgd_update
  *   gp_calib_p2p_copy       harness.py:552-557 beta probe (flood), on NVLink
  *   gp_calib_pingpong       harness.py:547-550 alpha probe (1-byte ping), on NVLink
- *   gp_comm_set_tuning / _set_trace / _info / _set_call_counter: no reference
- *                           counterpart (CTA budget + timeout, timeline stamps,
- *                           introspection, 32-bit sequence-wrap test hook)
+ *   gp_comm_set_tuning / _set_trace / _info / _set_call_counter, gp_ring_plan:
+ *                           no reference counterpart (CTA budget + timeout,
+ *                           timeline stamps, introspection, 32-bit sequence-wrap
+ *                           test hook, launch-plan query)
  *
  * Return value: GP_OK (0) or a GP_ERR_* code; gp_last_error_string() gives
  * the calling thread's last message. Failures detected on the device
@@ -102,6 +103,11 @@ int gp_comm_destroy(gp_comm* comm);
  * (sequence numbers cycle 1 .. 2^32-1; tests start near the wrap). Every rank
  * must set the same value while no call is in flight. */
 int gp_comm_set_call_counter(gp_comm* comm, uint64_t calls);
+/* Launch plan of a ring call (pure host logic, no GPU needed): out[0] chunk
+ * elements, out[1] CTAs launched, out[2] 1 = LL protocol, out[3] chunks in
+ * the largest phase, for n elements over `world` ranks, a communicator of
+ * `ctas` CTAs and `max_elems` capacity. */
+int gp_ring_plan(uint64_t n, int world, int ctas, int codec, int flags, uint64_t max_elems, int64_t* out);
 
 int gp_allreduce(gp_comm* comm, const float* in, float* out, uint64_t n, int codec,
                  uint32_t iteration, void* stream);

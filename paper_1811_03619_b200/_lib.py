@@ -25,7 +25,7 @@ GP_RING_PRECOMPRESS, GP_RING_SLOT_OUT = 1, 2
 EXPORTS = (
     "gp_comm_create", "gp_comm_create_emulated", "gp_comm_ipc_handle", "gp_comm_connect_ipc",
     "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_info", "gp_comm_destroy",
-    "gp_comm_set_call_counter",
+    "gp_comm_set_call_counter", "gp_ring_plan",
     "gp_allreduce", "gp_allreduce_ex", "gp_allreduce_emulated", "gp_allreduce_emulated_ex",
     "gp_gather_sum", "gp_broadcast", "gp_gather_sum_emulated", "gp_broadcast_emulated",
     "gp_comm_poll_error", "gp_get_stats",
@@ -57,6 +57,7 @@ _SIGS = {
     "gp_comm_set_trace": (_i, [_vp, _vp]),
     "gp_comm_info": (_i, [_vp, ctypes.POINTER(ctypes.c_int64)]),
     "gp_comm_set_call_counter": (_i, [_vp, ctypes.c_uint64]),
+    "gp_ring_plan": (_i, [_u64, _i, _i, _i, _i, _u64, ctypes.POINTER(ctypes.c_int64)]),
     "gp_comm_destroy": (_i, [_vp]),
     "gp_allreduce": (_i, [_vp, _vp, _vp, _u64, _i, _u32, _vp]),
     "gp_allreduce_emulated": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _u64, _i, _u32, _vp]),

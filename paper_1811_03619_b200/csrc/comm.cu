@@ -157,6 +157,30 @@ uint32_t pick_chunk(uint64_t n, int p, int G, int codec) {
   return (uint32_t)std::max(lo, std::min(hi, ch));
 }
 
+struct RingPlan {
+  uint32_t chunk;  // elements per chunk (from the communicator-wide G: every rank agrees)
+  int ctas;        // CTAs this call launches
+  int ll;          // LL protocol
+  uint64_t nch;    // chunks in the largest phase
+};
+
+// Launch plan of one ring call. Launch only as many warps as the largest
+// phase has chunks: the chunk size (and so every flag index) still follows
+// the communicator-wide G, but small calls no longer start G CTAs whose warps
+// would only hammer the phase counters (2p same-address atomics per idle
+// warp). LL when the block payload fits ll_payload_limit(p) and the slot.
+RingPlan plan_ring(uint64_t n, int p, int G, int codec, int pre, uint64_t ll_cap) {
+  RingPlan r{};
+  r.chunk = pick_chunk(n, p, G, codec);
+  const uint64_t maxblk = (n + p - 1) / p + 16;
+  r.nch = (maxblk + r.chunk - 1) / r.chunk;
+  if (pre && codec == GP_CODEC_QUANT8) r.nch = std::max<uint64_t>(r.nch, (n + r.chunk - 1) / r.chunk);
+  r.ctas = (int)std::min<uint64_t>((uint64_t)G, std::max<uint64_t>(1, (r.nch + kRingWarps - 1) / kRingWarps));
+  const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
+  r.ll = (maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), ll_cap)) ? 1 : 0;
+  return r;
+}
+
 int check_common(gp_comm* c, uint64_t n, int codec) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   if (codec < 0 || codec > 2) return fail(GP_ERR_ARG, "unknown codec " + std::to_string(codec));
@@ -308,6 +332,20 @@ int gp_comm_info(gp_comm* c, int64_t* o) {
   return GP_OK;
 }
 
+int gp_ring_plan(uint64_t n, int world, int ctas, int codec, int flags, uint64_t max_elems, int64_t* out) {
+  if (!out) return fail(GP_ERR_ARG, "null out");
+  if (world < 2 || world > kMaxRanks) return fail(GP_ERR_ARG, "world size must be in [2, 8]");
+  if (codec < 0 || codec > 2) return fail(GP_ERR_ARG, "unknown codec " + std::to_string(codec));
+  if (ctas < 1) return fail(GP_ERR_ARG, "ctas must be >= 1");
+  const Layout L = make_layout(world, std::max<uint64_t>(max_elems, n));
+  const RingPlan pl = plan_ring(n, world, ctas, codec, (flags & GP_RING_PRECOMPRESS) ? 1 : 0, L.ll_cap);
+  out[0] = pl.chunk;
+  out[1] = pl.ctas;
+  out[2] = pl.ll;
+  out[3] = (int64_t)pl.nch;
+  return GP_OK;
+}
+
 int gp_comm_set_call_counter(gp_comm* c, uint64_t calls) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   if (calls > 0xFFFFFFFFull) return fail(GP_ERR_ARG, "call counter holds a 32-bit sequence number");
@@ -380,18 +418,11 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
   P.pre = (flags & GP_RING_PRECOMPRESS) ? 1 : 0;
   ++c->seq;  // host-side count (info only); the kernel numbers calls on the device
   P.iteration = iteration;
-  P.chunk = pick_chunk(n, p, c->G, codec);
   {
-    // Launch only as many warps as the largest phase has chunks: the chunk
-    // size (and so every flag index) still follows the communicator-wide G,
-    // but small calls no longer start G CTAs whose warps would only hammer
-    // the phase counters (2p same-address atomics per idle warp).
-    const uint64_t maxblk = (n + p - 1) / p + 16;
-    uint64_t nch = (maxblk + P.chunk - 1) / P.chunk;
-    if (P.pre && codec == GP_CODEC_QUANT8) nch = std::max<uint64_t>(nch, (n + P.chunk - 1) / P.chunk);
-    P.G = (int)std::min<uint64_t>((uint64_t)c->G, std::max<uint64_t>(1, (nch + kRingWarps - 1) / kRingWarps));
-    const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
-    P.ll = (maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), c->L.ll_cap)) ? 1 : 0;
+    const RingPlan pl = plan_ring(n, p, c->G, codec, P.pre, c->L.ll_cap);
+    P.chunk = pl.chunk;
+    P.G = pl.ctas;
+    P.ll = pl.ll;
   }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;

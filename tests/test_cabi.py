@@ -84,3 +84,36 @@ def test_argument_errors_are_reported_without_a_gpu():
         assert msg in lib.gp_last_error_string().decode()
     with pytest.raises(ConfigError, match="unknown codec"):
         _lib.call("gp_encode", 9, p, 8, p, p, None)
+
+
+def _plan(n, world, ctas, codec, flags=0, max_elems=None):
+    from paper_1811_03619_b200 import _lib
+    out = (ctypes.c_int64 * 4)()
+    _lib.call("gp_ring_plan", n, world, ctas, codec, flags, max_elems or n, out)
+    return {"chunk": out[0], "ctas": out[1], "ll": out[2], "nch": out[3]}
+
+
+@pytest.mark.parametrize("world,codec", [(2, 0), (2, 1), (2, 2), (4, 0), (4, 1), (8, 0), (8, 2)])
+def test_ll_protocol_threshold(world, codec):
+    """LL iff the block payload (incl. 16 elements of slack) fits
+    512 KiB x (p - 1), capped at 2 MiB (ring.cuh:ll_payload_limit)."""
+    w = (4, 2, 1)[codec]
+    limit = min((512 << 10) * (world - 1), 2 << 20)
+    n_max = world * (limit // w - 16)  # largest n whose ceil(n/p) + 16 blocks fit
+    assert _plan(n_max, world, 592, codec)["ll"] == 1
+    assert _plan(n_max + world, world, 592, codec)["ll"] == 0
+    assert _plan(1, world, 592, codec)["ll"] == 1
+
+
+def test_launch_and_chunk_plan():
+    # tiny calls launch one CTA; the chunk stays at its 1024-element minimum
+    assert _plan(8, 2, 592, 1) == {"chunk": 1024, "ctas": 1, "ll": 1, "nch": 1}
+    # C2 gradient, standalone budget: 1024-element chunks, one per warp
+    pl = _plan(4_710_538, 2, 592, 1)
+    assert pl["chunk"] == 1024 and pl["nch"] == 2301 and pl["ctas"] == 576 and pl["ll"] == 0
+    # the engine's 256-CTA budget: bigger chunks, fewer of them, still one per warp
+    pl = _plan(4_710_538, 2, 256, 1)
+    assert pl["chunk"] == 3072 and pl["ctas"] == 192
+    # quant8 with the fused pre-compress scans the whole vector in chunk units
+    a, b = _plan(1_000_000, 4, 592, 2), _plan(1_000_000, 4, 592, 2, flags=1)
+    assert b["nch"] >= 4 * a["nch"] - 4
