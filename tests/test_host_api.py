@@ -1,0 +1,103 @@
+"""CPU tests of the host-side API mirror (no GPU): RunConfig validation
+(engine.py:80-107), effective_mode (:132-136), partition_blocks
+(collective.py:35-49), Codec.parse (compression.py:44-49). Where
+/root/reference is mounted (the build container) every answer is also
+compared with the reference package itself."""
+
+import importlib
+import os
+import sys
+
+import pytest
+
+from oracle import ring as OR
+
+REF = "/root/reference/pkg/src"
+
+
+def ref_module(name):
+    if not os.path.isdir(REF):
+        return None
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    try:
+        return importlib.import_module(f"gradpipe.{name}")
+    except Exception:  # noqa: BLE001 - reference unavailable: skip the comparison
+        return None
+
+
+BAD_CONFIGS = [
+    dict(mode="bogus"),
+    dict(iterations=0),
+    dict(learning_rate=0.0),
+    dict(learning_rate=-1.0),
+    dict(mode="pipe_sgd", depth=1),
+    dict(batch_size=0),
+    dict(warmup_epochs=-1),
+    dict(eval_interval=-1),
+]
+
+
+@pytest.mark.parametrize("kw", BAD_CONFIGS)
+def test_runconfig_rejects_what_the_reference_rejects(kw):
+    from paper_1811_03619_b200.engine import RunConfig
+    from paper_1811_03619_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        RunConfig(**kw)
+    ref = ref_module("engine")
+    if ref is not None:
+        with pytest.raises(Exception):
+            ref.RunConfig(**kw)
+
+
+def test_runconfig_defaults_and_codec_names():
+    from paper_1811_03619_b200.compression import Codec
+    from paper_1811_03619_b200.engine import RunConfig
+    c = RunConfig(mode="pipe_sgd", codec="trunc16")
+    assert c.codec is Codec.TRUNC16 and c.depth == 2
+    ref = ref_module("engine")
+    if ref is not None:
+        r = ref.RunConfig(mode="pipe_sgd")
+        for f in ("iterations", "learning_rate", "depth", "batch_size", "warmup_epochs", "eval_interval",
+                  "seed", "lr_decay_every", "lr_decay_factor", "snapshot_first"):
+            assert getattr(r, f) == getattr(RunConfig(mode="pipe_sgd"), f), f
+
+
+@pytest.mark.parametrize("name", ["none", "NONE", " trunc16 ", "quant8", "Quant8"])
+def test_codec_parse_matches_reference(name):
+    from paper_1811_03619_b200.compression import Codec
+    ours = Codec.parse(name)
+    ref = ref_module("compression")
+    if ref is not None:
+        assert int(ref.Codec.parse(name)) == int(ours)
+
+
+def test_codec_parse_rejects_unknown():
+    from paper_1811_03619_b200.compression import Codec
+    from paper_1811_03619_b200.errors import CodecError
+    with pytest.raises(CodecError):
+        Codec.parse("fp8")
+
+
+@pytest.mark.parametrize("warmup", [0, 1, 3])
+def test_effective_mode_warmup_switch(warmup):
+    from paper_1811_03619_b200.engine import RunConfig, effective_mode
+    c = RunConfig(mode="pipe_sgd", warmup_epochs=warmup)
+    got = [effective_mode(c, e) for e in range(5)]
+    assert got == ["d_sync"] * min(warmup, 5) + ["pipe_sgd"] * (5 - min(warmup, 5))
+    ref = ref_module("engine")
+    if ref is not None:
+        rc = ref.RunConfig(mode="pipe_sgd", warmup_epochs=warmup)
+        assert [str(ref.effective_mode(rc, e)) for e in range(5)] == got
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 7, 8])
+def test_partition_blocks_all_shapes(p):
+    from paper_1811_03619_b200.collective import partition_blocks
+    for n in (0, 1, p - 1, p, p + 1, 1000, 4099, 61_100_840):
+        got = partition_blocks(n, p)
+        assert got == OR.partition_blocks(n, p)
+        assert sum(length for _, length in got) == n
+        ref = ref_module("collective")
+        if ref is not None:
+            assert [tuple(b) for b in ref.partition_blocks(n, p)] == got
