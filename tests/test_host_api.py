@@ -101,3 +101,23 @@ def test_partition_blocks_all_shapes(p):
         ref = ref_module("collective")
         if ref is not None:
             assert [tuple(b) for b in ref.partition_blocks(n, p)] == got
+
+
+def test_gradient_buffer_contract():
+    """engine.py:188-235: slot tag % K, written once, take clears. The
+    reference's take blocks until the comm thread puts; here puts are
+    stream-ordered before takes on the host, so a missing slot is an error."""
+    from paper_1811_03619_b200.engine import GradientBuffer
+    from paper_1811_03619_b200.errors import EngineError
+    b = GradientBuffer(2)
+    b.put(-2, "zero-a")
+    b.put(-1, "zero-b")
+    with pytest.raises(EngineError, match="written twice"):
+        b.put(0, "t0")  # slot 0 still holds tag -2
+    assert b.take(-2) == "zero-a"
+    b.put(0, "t0")
+    with pytest.raises(EngineError, match="holds iteration"):
+        b.take(2)  # slot 0 holds tag 0, not 2
+    assert b.take(0) == "t0"
+    with pytest.raises(EngineError, match="never produced"):
+        b.take(0)
