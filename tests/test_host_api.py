@@ -121,3 +121,20 @@ def test_gradient_buffer_contract():
     assert b.take(0) == "t0"
     with pytest.raises(EngineError, match="never produced"):
         b.take(0)
+
+
+@pytest.mark.parametrize("codec", ["none", "trunc16", "quant8"])
+def test_wire_and_payload_sizes_match_reference(codec):
+    """compression.py:33, :154-172: 9-byte header + n x width payload."""
+    from paper_1811_03619_b200.compression import Codec, payload_size, wire_size
+    from paper_1811_03619_b200.errors import CodecError
+    c = Codec.parse(codec)
+    ref = ref_module("compression")
+    for n in (0, 1, 7, 4099, 61_100_840):
+        assert wire_size(c, n) == 9 + payload_size(c, n) == 9 + n * c.bytes_per_elem
+        if ref is not None:
+            rc = ref.Codec.parse(codec)
+            assert ref.wire_size(rc, n) == wire_size(c, n)
+            assert ref.payload_size(rc, n) == payload_size(c, n)
+    with pytest.raises(CodecError):
+        payload_size(c, -1)
