@@ -117,3 +117,24 @@ def test_launch_and_chunk_plan():
     # quant8 with the fused pre-compress scans the whole vector in chunk units
     a, b = _plan(1_000_000, 4, 592, 2), _plan(1_000_000, 4, 592, 2, flags=1)
     assert b["nch"] >= 4 * a["nch"] - 4
+
+
+def test_plain_c_client_compiles_links_and_runs(tmp_path):
+    """include/pipesgd.h is plain C: a C11 program using it compiles with gcc,
+    links against libpipesgd.so and gets plans and error codes without a GPU."""
+    import shutil
+    import subprocess
+    from paper_1811_03619_b200 import _lib
+    lib = _lib.load()._name
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    exe = tmp_path / "c_abi_client"
+    libdir = os.path.dirname(lib)
+    subprocess.run([gcc, "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_abi_client.c"), "-L", libdir, "-l:" + os.path.basename(lib),
+                    "-Wl,-rpath," + libdir, "-o", str(exe)], check=True, capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "chunk=1024 ctas=576 ll=0 nch=2301" in r.stdout
+    assert "errors ok" in r.stdout
