@@ -4,15 +4,19 @@ ring AllReduce on B200, plus ring bus bandwidth, roofline and CPU baselines.
     python bench.py [--gpus 1] [--steps 30] [--warmup 5]
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
         --master-port P bench.py --gpus N --steps K --warmup W
-    python bench.py --impl reference ...     # the reference's CPU path (oracle port)
+    python bench.py --impl reference ...     # the reference's CPU path (baseline/_ref)
 
-Workload (BASELINE.json configs[1], "C2"): CIFAR-10-shaped small CNN
-(4,710,538 fp32 params), Pipe-SGD width 2, trunc16 ring compression, fixed
-global batch split over N GPUs (strong scaling, as in the paper's setup).
-One step = one Pipe-SGD iteration on every rank: consume the aggregated
-gradient of t-2 (decode, /p, SGD), forward+backward on the rank's batch,
-whole-vector D(C(grad)), fused compressed ring AllReduce on the comm stream,
-whole-vector re-compress of the sum into slot t. Prints ONE JSON line (rank 0).
+Workload (BASELINE.json configs[2], "C3", the largest configuration that
+fits one GPU): AlexNet-shaped (torchvision AlexNet, 61,100,840 fp32 params,
+ImageNet-shaped 3x224x224 synthetic batch, global batch 256 as in the paper,
+PAPER.md:250) trained with Pipe-SGD width 2 and 8-bit quantized ring
+compression; the fixed global batch is split over N GPUs (strong scaling,
+as in the paper's setup). One step = one Pipe-SGD iteration on every rank:
+consume the aggregated gradient of t-2 (decode, /p, SGD), forward+backward
+on the rank's batch, whole-vector D(C(grad)), fused compressed ring
+AllReduce on the comm stream, whole-vector re-compress of the sum into
+slot t. Prints ONE JSON line (rank 0). `--model c1|c2|c4` selects the other
+BASELINE configs (each with its codec and global batch by default).
 """
 
 from __future__ import annotations
@@ -43,11 +47,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--model", default="c2")
-    ap.add_argument("--codec", default="trunc16")
+    ap.add_argument("--model", default="c3")
+    ap.add_argument("--codec", default=None, help="default: the config's codec (BASELINE.json configs)")
     ap.add_argument("--mode", default="pipe_sgd")
     ap.add_argument("--depth", type=int, default=2)
-    ap.add_argument("--global-batch", type=int, default=512)
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="default: the paper's global batch for the config (100 MNIST, 512 CIFAR, 256 ImageNet)")
     ap.add_argument("--ctas", type=int, default=256,
                     help="128-thread CTAs the ring kernel may occupy per GPU beside the compute stream")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -59,7 +64,17 @@ def parse():
                     help="feed NHWC activations to cuDNN (no NCHW<->NHWC transposes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-allreduce-sweep", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    dflt = CONFIG_DEFAULTS.get(a.model, ("none", 256))
+    if a.codec is None:
+        a.codec = dflt[0]
+    if a.global_batch is None:
+        a.global_batch = dflt[1]
+    return a
+
+
+# BASELINE.json configs: codec and global batch per model
+CONFIG_DEFAULTS = {"c1": ("none", 100), "c2": ("trunc16", 512), "c3": ("quant8", 256), "c4": ("none", 256)}
 
 
 # ------------------------------------------------------------------ helpers
@@ -189,108 +204,158 @@ def cpu_model():
 
 # ------------------------------------------------- the reference's CPU path
 
-def oracle_iteration(grads, w, codec, p, lr, state, pool=None):
-    """One Pipe-SGD iteration of the reference's hot path, restated by the
-    oracle (engine.py:333/:355 local D(C(g)), collective.py ring, engine.py:407
-    re-compress, :420-426 decompress, :123-129 mean, models.py:198-204 SGD).
-    Consumes the slot of t-2, produces slot t (width 2). The p ranks' local
-    compressions run on `pool` (one thread per rank, as the reference's rank
-    threads; numpy releases the GIL inside them); the replica-identical
-    re-compress and update run once."""
-    from oracle import codec as OC
-    from oracle import engine as OE
-    from oracle import ring as OR
-    if pool is not None and p > 1:
-        local = list(pool.map(lambda g: OC.roundtrip(g, codec), grads))
-    else:
-        local = [OC.roundtrip(g, codec) for g in grads]
-    summed = OR.ring_allreduce_all(local, codec).outputs[0] if p > 1 else local[0].copy()
-    state.append(OC.encode(summed, codec))
-    slot = state.pop(0)
-    agg = OC.decode(codec, *slot)
-    return OE.sgd_update(w, OE.aggregate_mean(agg, p), lr)
+def load_reference():
+    """The unmodified reference package, installed into baseline/_ref
+    (git-ignored; it travels to the GPU box with the repo snapshot):
+    `pip install --no-index --no-deps --target baseline/_ref <copy of
+    /root/reference/pkg>`. None when absent (then the oracle port stands in)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "gradpipe")):
+        return None
+    if path not in sys.path:
+        sys.path.append(path)
+    try:
+        import gradpipe  # noqa: F401
+        from gradpipe import collective, compression, engine, models, transport  # noqa: F401
+    except Exception:  # noqa: BLE001 - a broken install is reported as absent
+        return None
+    import gradpipe
+    return gradpipe
 
 
-class CpuPath:
-    """The reference path on this host's CPU for an n-element gradient and p
-    simulated ranks (one thread, numpy, inputs generated once)."""
+class RefPath:
+    """The reference's per-iteration Pipe-SGD hot path on this host's CPU,
+    p ranks as threads of one process exactly like run_inproc_cluster
+    (engine.py:563-618), for an n-element gradient. Per rank and step:
+      decompress(slot[t-K]) -> aggregate_mean -> sgd_update   (engine.py:420-426, :302-307)
+      compress(grad)                                          (engine.py:333)
+      ring_allreduce(decompress(block)) over InProcTransport  (engine.py:399-406)
+      compress(summed) into slot t                            (engine.py:407)
+    The model's forward/backward is not part of it: the reference has no
+    CNN (models.py has logistic / MLP only), so this flatters the reference.
+    Uses the real reference package when baseline/_ref holds it (kind
+    "reference"), else the oracle's restatement of it (kind "port")."""
 
-    def __init__(self, n, p, codec):
+    def __init__(self, n, p, codec_name, depth=2, seed=0):
         from concurrent.futures import ThreadPoolExecutor
+        self.ref = load_reference()
+        self.kind = "reference" if self.ref is not None else "port"
+        self.n, self.p, self.depth = n, p, depth
+        g = np.random.default_rng(seed)
+        self.grads = [g.normal(0, 1e-2, n).astype(np.float32) for _ in range(p)]
+        w0 = g.normal(0, 0.05, n).astype(np.float32)
+        self.w = [w0.copy() for _ in range(p)]
+        self.t = 1
+        if self.ref is not None:
+            from gradpipe import compression as RC
+            from gradpipe import transport as RT
+            self.codec = RC.Codec.parse(codec_name)
+            zero = RC.compress(np.zeros(n, np.float32), self.codec)
+            self.tr = RT.InProcTransport(p)
+        else:
+            from oracle import codec as OC
+            self.codec = {"none": OC.NONE, "trunc16": OC.TRUNC16, "quant8": OC.QUANT8}[codec_name]
+            zero = OC.encode(np.zeros(n, np.float32), self.codec)
+            self.tr = None
+        self.slots = [[zero] * depth for _ in range(p)]
+        self.threads = p
+        self.pool = ThreadPoolExecutor(p) if p > 1 else None
+
+    def _rank_step_ref(self, r):
+        from gradpipe import collective as RCo
+        from gradpipe import compression as RC
+        from gradpipe import engine as RE
+        from gradpipe import models as RM
+        t, p = self.t, self.p
+        total = RC.decompress(self.slots[r].pop(0))
+        self.w[r] = RM.sgd_update(self.w[r], RE.aggregate_mean(total, p), 0.05)
+        block = RC.compress(self.grads[r], self.codec)
+        summed = RCo.ring_allreduce(RC.decompress(block), r, p, self.tr.endpoint(r), self.codec, iteration=t)
+        self.slots[r].append(RC.compress(summed, self.codec))
+
+    def _step_port(self):
         from oracle import codec as OC
-        g = np.random.default_rng(0)
-        self.grads = [(g.normal(0, 1e-2, n)).astype(np.float32) for _ in range(p)]
-        self.w = g.normal(0, 0.05, n).astype(np.float32)
-        zero = OC.encode(np.zeros(n, np.float32), codec)
-        self.state = [zero, zero]
-        self.p, self.codec = p, codec
-        self.threads = max(1, min(p, os.cpu_count() or 1))
-        self.pool = ThreadPoolExecutor(self.threads) if self.threads > 1 else None
+        from oracle import engine as OE
+        from oracle import ring as OR
+        p = self.p
+        for r in range(p):
+            total = OC.decode(self.codec, *self.slots[r].pop(0))
+            self.w[r] = OE.sgd_update(self.w[r], OE.aggregate_mean(total, p), 0.05)
+        if self.pool is not None:
+            local = list(self.pool.map(lambda g: OC.roundtrip(g, self.codec), self.grads))
+        else:
+            local = [OC.roundtrip(g, self.codec) for g in self.grads]
+        summed = OR.ring_allreduce_all(local, self.codec).outputs[0] if p > 1 else local[0].copy()
+        for r in range(p):
+            self.slots[r].append(OC.encode(summed, self.codec))
 
     def step(self):
-        self.w = oracle_iteration(self.grads, self.w, self.codec, self.p, 0.05, self.state, self.pool)
+        if self.ref is None:
+            self._step_port()
+        elif self.pool is not None:
+            list(self.pool.map(self._rank_step_ref, range(self.p)))
+        else:
+            self._rank_step_ref(0)
+        self.t += 1
 
 
-def cpu_path_rate(n, p, codec, seconds, max_iters=1000):
-    """Iterations/s of the reference path on this host, bounded to `seconds`."""
-    cp = CpuPath(n, p, codec)
-    cp.step()  # warm
+def ref_sample_size(n, p, codec_name, seconds_per_step):
+    """Elements per reference step so one step takes about `seconds_per_step`:
+    the per-element cost measured on a 2^20-element probe of the same path.
+    The bounded sample is a contiguous slice of the gradient; the path is
+    elementwise (its cost is linear in n), so iters/s = (n_s / n) / t_step."""
+    m = min(n, 1 << 20)
+    probe = RefPath(m, p, codec_name)
+    probe.step()
     t0 = time.perf_counter()
-    k = 0
-    while k < max_iters and (k < 2 or time.perf_counter() - t0 < seconds):
-        cp.step()
-        k += 1
-    dt = time.perf_counter() - t0
-    return k / dt, k, dt
+    probe.step()
+    per_elem = (time.perf_counter() - t0) / m
+    ns = int(min(n, max(m, seconds_per_step / max(per_elem, 1e-12))))
+    return max(p * 16, ns - ns % (p * 16)) if ns < n else n
 
 
-def cpu_ring_times(n, codec, codec_name, ps=(2, 4)):
-    """The reference ring_allreduce (oracle port, collective.py:77-163) on
-    this host for the step's gradient: all p ranks simulated in one thread,
-    one call each (the SURVEY 8(d) CPU path beside the GPU ring)."""
-    from oracle.ring import ring_allreduce_all
-    g = np.random.default_rng(1)
-    out = []
-    for p in ps:
-        xs = [g.normal(0, 1e-2, n).astype(np.float32) for _ in range(p)]
+def reference_rate(n, p, codec_name, steps, warmup, seconds_per_step=2.0):
+    """iters/s of the reference path (scaled from the bounded sample), and the sample."""
+    ns = ref_sample_size(n, p, codec_name, seconds_per_step)
+    rp = RefPath(ns, p, codec_name)
+    for _ in range(warmup):
+        rp.step()
+    per = []
+    for _ in range(steps):
         t0 = time.perf_counter()
-        ring_allreduce_all(xs, codec)
-        dt = time.perf_counter() - t0
-        out.append({"p": p, "n": n, "codec": codec_name, "s_per_call_all_ranks": dt,
-                    "busbw_fp32_gbs": 2 * (p - 1) / p * 4 * n / dt / 1e9})
-    return out
+        rp.step()
+        per.append(time.perf_counter() - t0)
+    t = float(np.mean(per))
+    return (ns / n) / t, rp, ns, t
+
+
+def ref_sample_text(rp, n, ns, t, steps, codec_name):
+    who = ("the unmodified reference package (baseline/_ref/gradpipe: compression.compress/decompress, "
+           "collective.ring_allreduce over transport.InProcTransport, engine.aggregate_mean, "
+           "models.sgd_update)" if rp.kind == "reference" else "the oracle's restatement of the reference path")
+    frac = "the full gradient" if ns == n else f"a {ns}-element slice ({ns / n:.3f}) of the {n}-element gradient, " \
+                                              f"iters/s scaled by that fraction (the path is elementwise)"
+    return (f"{who}: per step and rank decompress(slot t-2) -> mean -> SGD, compress({codec_name}) of the local "
+            f"gradient, ring_allreduce over p={rp.p} ranks as threads, compress of the sum; {frac}; {steps} steps "
+            f"of {t:.2f} s; no forward/backward (the reference has no CNN: flatters the reference); "
+            f"host {cpu_model()}, {os.cpu_count()} cpus")
 
 
 def reference_arm(args, ws, rank):
     if rank != 0:
         return None
-    from oracle import codec as OC
     from paper_1811_03619_b200.models import build_torch_model
     mod, _, _ = build_torch_model(args.model)
     n = sum(p.numel() for p in mod.parameters())
-    codec = {"none": OC.NONE, "trunc16": OC.TRUNC16, "quant8": OC.QUANT8}[args.codec]
     p = max(1, args.gpus)
-    cp = CpuPath(n, p, codec)
-    for _ in range(args.warmup):
-        cp.step()
-    per_step = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cp.step()
-        per_step.append(time.perf_counter() - t0)
-    t = float(np.mean(per_step))
-    v = 1.0 / t
-    sample = (f"oracle port of the reference hot path (gradpipe codec {args.codec} on the whole "
-              f"{n}-element gradient, ring_allreduce over p={p} simulated ranks, whole-vector re-compress, "
-              f"mean, SGD) per step, numpy, {cp.threads} thread(s): the ranks' local compressions in "
-              f"parallel like the reference's rank threads, the replica-identical rest once; the reference "
-              f"has no CNN so forward/backward is excluded (flatters the reference); host: {cpu_model()}, "
-              f"{os.cpu_count()} cpus")
+    v, rp, ns, t = reference_rate(n, p, args.codec, args.steps, args.warmup)
+    sample = ref_sample_text(rp, n, ns, t, args.steps, args.codec)
     return {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": workload_config(args, n, args.gpus),
-            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cp.threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": rp.threads, "kind": rp.kind,
+                             "sample": sample},
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -600,7 +665,7 @@ def our_arm(args, ws, rank, local):
         line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": N, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic (random CIFAR-shaped images/labels, random-init weights)",
+                "data": f"synthetic (random {'x'.join(map(str, in_shape))} inputs and labels, random-init weights)",
                 "config": workload_config(args, n, N),
                 "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d * N,
                         "d2h_bytes_per_step": 4 * N,
@@ -841,15 +906,20 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = our_arm(args, ws, rank, local)
     if line is not None and not args.no_cpu_baseline and ws == 1:
-        from oracle import codec as OC
-        codec = {"none": OC.NONE, "trunc16": OC.TRUNC16, "quant8": OC.QUANT8}[args.codec]
-        v, k, dt = cpu_path_rate(line["config"]["params"], 1, codec, args.cpu_seconds)
-        line["cpu_baseline"] = {
-            "value": v, "unit": "iters/s", "cores": 1, "kind": "port",
-            "sample": (f"{k} iterations ({dt:.1f} s) of the oracle port of the reference hot path on the "
-                       f"{line['config']['params']}-element gradient (codec, p=1 ring, re-compress, mean, SGD; "
-                       f"no CNN fwd/bwd: the reference has none); host {cpu_model()}"),
-            "ring_allreduce": cpu_ring_times(line["config"]["params"], codec, args.codec)}
+        n = line["config"]["params"]
+        steps = 5
+        v, rp, ns, t = reference_rate(n, 1, args.codec, steps, 1, seconds_per_step=args.cpu_seconds / steps)
+        line["cpu_baseline"] = {"value": v, "unit": "iters/s", "cores": rp.threads, "kind": rp.kind,
+                                "sample": ref_sample_text(rp, n, ns, t, steps, args.codec)}
+        # the same work on both sides: our kernels' device time per step (the
+        # update + the comm stream's codec / ring kernels) vs the reference's
+        # CPU time per step for the identical path
+        ours_ms = sum(line["kernels"][k]["in_pipeline_avg_ms"] or 0.0 for k in line["kernels"]
+                      if k in ("update", "compress", "recompress", "ring"))
+        line["hot_path_per_step"] = {
+            "gpu_ms": ours_ms, "cpu_reference_ms": 1e3 / v, "speedup": (1e3 / v) / ours_ms if ours_ms else None,
+            "what": "decode(slot t-2) + mean + SGD, whole-vector compress of the gradient, ring (identity at "
+                    "p = 1), compress of the sum: our kernels' in-step device time vs the reference's CPU time"}
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -105,8 +105,10 @@ int gp_comm_destroy(gp_comm* comm);
 int gp_comm_set_call_counter(gp_comm* comm, uint64_t calls);
 /* Launch plan of a ring call (pure host logic, no GPU needed): out[0] chunk
  * elements, out[1] CTAs launched, out[2] 1 = LL protocol, out[3] chunks in
- * the largest phase, for n elements over `world` ranks, a communicator of
- * `ctas` CTAs and `max_elems` capacity. */
+ * the largest phase, out[4] 1 = direct reduce-scatter (codec none, world >= 3:
+ * every rank pushes each block straight to its owner, who folds them in the
+ * ring's order), for n elements over `world` ranks, a communicator of
+ * `ctas` CTAs and `max_elems` capacity. `out` holds 5 int64. */
 int gp_ring_plan(uint64_t n, int world, int ctas, int codec, int flags, uint64_t max_elems, int64_t* out);
 
 int gp_allreduce(gp_comm* comm, const float* in, float* out, uint64_t n, int codec,

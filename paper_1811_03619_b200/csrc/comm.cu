@@ -162,6 +162,7 @@ struct RingPlan {
   int ctas;        // CTAs this call launches
   int ll;          // LL protocol
   uint64_t nch;    // chunks in the largest phase
+  int direct;      // codec none, p >= 3: direct reduce-scatter (one hop instead of p - 1)
 };
 
 // Launch plan of one ring call. Launch only as many warps as the largest
@@ -178,6 +179,11 @@ RingPlan plan_ring(uint64_t n, int p, int G, int codec, int pre, uint64_t ll_cap
   r.ctas = (int)std::min<uint64_t>((uint64_t)G, std::max<uint64_t>(1, (r.nch + kRingWarps - 1) / kRingWarps));
   const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
   r.ll = (maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), ll_cap)) ? 1 : 0;
+  // codec none folds D(C(.)) = identity, so the owner can fold every rank's
+  // raw block in the ring's order after one NVSwitch hop: bit-identical
+  // sums, identical wire bytes; PIPESGD_DIRECT=0 keeps the ring
+  static const uint64_t direct_on = env_u64("PIPESGD_DIRECT", 1);
+  r.direct = (direct_on && codec == GP_CODEC_NONE && p >= 3) ? 1 : 0;
   return r;
 }
 
@@ -343,6 +349,7 @@ int gp_ring_plan(uint64_t n, int world, int ctas, int codec, int flags, uint64_t
   out[1] = pl.ctas;
   out[2] = pl.ll;
   out[3] = (int64_t)pl.nch;
+  out[4] = pl.direct;
   return GP_OK;
 }
 
@@ -423,6 +430,7 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
     P.chunk = pl.chunk;
     P.G = pl.ctas;
     P.ll = pl.ll;
+    P.direct = pl.direct;
   }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;
@@ -515,6 +523,7 @@ static int star(gp_comm* c, const float* const* ins, float* const* outs, uint64_
   S.mode = mode;
   S.zero_first = zero_first;
   S.ctas = std::max(1, c->G / 4);
+  S.max_ctas = std::max(1, sm_count(c->device) * std::max(1, 8 / c->nlocal));
   S.nlocal = c->nlocal;
   for (int i = 0; i < c->nlocal; ++i) {
     const int r = c->nlocal == 1 ? c->rank : i;
@@ -591,8 +600,8 @@ int gp_comm_poll_error(gp_comm* c, gp_error* out) {
   }
   if (best != ~0ull) {
     static const int phases[4] = {kPhRS, kPhBarrier, kPhAG, kPhLocal};
-    out->phase = phases[(best >> 60) & 0xF];
-    out->step = (int)((best >> 53) & 0x7F);  // bit 52: abort consequence (ordering only)
+    out->phase = phases[(best >> 60) & 0x7];  // bit 63: abort consequence (ordering only)
+    out->step = (int)((best >> 53) & 0x7F);
     out->kind = (int)((best >> 48) & 0xF);
     out->block = (int)((best >> 40) & 0xFF) - 1;
     out->rank = (int)((best >> 32) & 0xFF);

@@ -22,9 +22,12 @@ enum Phase : int { kPhRS = 0, kPhAG = 1, kPhBarrier = 2, kPhLocal = 3 };
 
 // Device error word: one u64 so the EARLIEST failure wins via atomicMin,
 // ordered by (phase order, step) like the reference, which fails at the
-// first step that cannot complete. 0 = no error.
-//   [63:60] phase order (0 reduce-scatter, 1 barrier, 2 allgather, 3 local)
-//   [59:52] step   [51:48] kind   [47:40] block+1   [39:32] rank   [31:0] detail
+// first step that cannot complete. 0xFF..F = no error.
+//   [63] consequence (a wait that only ended because a peer aborted: any
+//        cause this rank detected itself -- timeout, header, non-finite --
+//        beats every consequence)
+//   [62:60] phase order (0 reduce-scatter, 1 barrier, 2 allgather, 3 local)
+//   [59:53] step   [51:48] kind   [47:40] block+1   [39:32] rank   [31:0] detail
 struct ErrWord {
   unsigned long long code;
   unsigned long long pad[3];
@@ -62,16 +65,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// Record a failure; the earliest (phase, step) is kept, and at the same
-// (phase, step) a cause (header mismatch, own timeout, non-finite) beats a
-// wait that only ended because a peer aborted (timeout kind, detail 1): bit
-// 52 marks those consequences. Steps fit 7 bits (p <= 8).
+// Record a failure; the earliest (phase, step) is kept among this rank's own
+// causes (header mismatch, own timeout, non-finite); a wait that only ended
+// because a peer aborted (timeout kind, detail 1) is reported only when the
+// rank has no cause of its own. Steps fit 7 bits (p <= 8).
 __device__ __forceinline__ void latch_error(ErrWord* e, int kind, int phase, int step, int block,
                                             int rank, int detail) {
   const unsigned long long consequence = (kind == kErrTimeout && detail == 1) ? 1ull : 0ull;
   const unsigned long long code =
-      ((unsigned long long)(phase_order(phase) & 0xF) << 60) | ((unsigned long long)(step & 0x7F) << 53) |
-      (consequence << 52) |
+      (consequence << 63) | ((unsigned long long)(phase_order(phase) & 0x7) << 60) |
+      ((unsigned long long)(step & 0x7F) << 53) |
       ((unsigned long long)(kind & 0xF) << 48) | ((unsigned long long)((block + 1) & 0xFF) << 40) |
       ((unsigned long long)(rank & 0xFF) << 32) | (unsigned long long)(uint32_t)detail;
   atomicMin(&e->code, code);

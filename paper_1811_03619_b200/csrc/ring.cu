@@ -122,18 +122,13 @@ __device__ __forceinline__ uint8_t* ll_line(uint8_t* llslot, uint64_t rel0) {
   return llslot + 32 + (rel0 / CodecT<C>::E) * 32;
 }
 
-// Abort this call on every rank: peers' spins see it and stop waiting.
+// Abort on every rank: peers' spins see it and stop waiting, and the abort
+// stays (ring.cuh:kAbortSticky), so later calls end at once too.
 __device__ void broadcast_abort(const RingParams& P, const RankCtx& R) {
-  for (int q = 0; q < P.p; ++q) {
-    Ctl* c = reinterpret_cast<Ctl*>(R.peer[q] + P.L.off_ctl);
-    atomicExch(&c->abort, (unsigned long long)s_seq);
-  }
-  fence_sys();
+  abort_all(R.peer, P.p, P.L.off_ctl, s_seq, R.rank);
 }
 
-__device__ __forceinline__ bool aborted(const RingParams& P, Ctl* ctl) {
-  return (uint32_t)(*(volatile unsigned long long*)&ctl->abort) == s_seq;
-}
+__device__ __forceinline__ bool aborted(const RingParams&, Ctl* ctl) { return comm_aborted(ctl); }
 
 // Flag word: (call sequence << 32) | quant8 scale bits. Carrying the scale in
 // the flag means no chunk has to read (or write) a shared header line.
@@ -157,7 +152,7 @@ __device__ uint64_t spin_flag(const uint64_t* f, const RingParams& P, const Rank
     if (ns < 256) ns <<= 1;
     if ((it & 63u) == 0) {
       if (aborted(P, ctl)) {
-        latch_error(err, kErrTimeout, phase, step, block, R.rank, 1 /* peer aborted */);
+        latch_error(err, kErrTimeout, phase, step, block, R.rank, abort_detail(ctl, R.rank));
         return 0;
       }
       if (globaltimer() - t0 > P.timeout_ns) {
@@ -235,6 +230,10 @@ __device__ __forceinline__ void warp_publish_all(const RingParams& P, const Rank
 // block max. Returns false on abort/timeout.
 __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err, int k,
                                  uint32_t mymax, float& vmax, int step) {
+  // every lane's pass-A stores (the partials in `out`) must be ordered
+  // before lane 0's arrival: __syncwarp orders them within the warp, and
+  // lane 0's fence below is cumulative over what it has observed
+  __syncwarp();
   const uint32_t m = warp_max_u32(mymax);
   int ok = 1;
   float v = 0.f;
@@ -247,7 +246,11 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
     for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->bar)) < target; ++it) {
       __nanosleep(64);
       if ((it & 63u) == 0) {
-        if (aborted(P, ctl)) { ok = 0; break; }
+        if (aborted(P, ctl)) {
+          latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, abort_detail(ctl, R.rank));
+          ok = 0;
+          break;
+        }
         if (globaltimer() - t0 > P.timeout_ns) {
           latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, 0);
           broadcast_abort(P, R);
@@ -310,16 +313,18 @@ __device__ __forceinline__ void stamp2(const RingParams& P, uint32_t wid, int lr
   if (on && P.p == 2) stamp(P, wid, lrank, k);
 }
 
-// Dynamic chunk scheduling: the warps of one rank take chunk indices of a
-// phase from a counter in the rank's control block (reset when the call
-// closes). Flags are per chunk, not per warp, so ranks need not agree on
-// which warp handles which chunk; fast warps take more chunks, which evens
-// out the unequal NVLink shares warps get under arbitration.
+// Chunk scheduling: in every phase warp w first takes chunk w (no atomic,
+// so a small call's warps never wait on the counter), then further chunks
+// from a counter in the rank's control block (reset when the call closes),
+// offset by the rank's warp count NW. Flags are per chunk, not per warp, so
+// ranks need not agree on which warp handles which chunk; fast warps take
+// more chunks, which evens out the unequal NVLink shares warps get under
+// arbitration.
 // Phases: 0 quant8 step-0 max, 1 step-0 send, 2+2s fold of step s,
 // 3+2s quant8 push of step s, 20+k allgather of the k-th block.
-__device__ __forceinline__ uint32_t grab(Ctl* ctl, int phase) {
+__device__ __forceinline__ uint32_t grab(Ctl* ctl, int phase, uint32_t nw) {
   uint32_t c = 0;
-  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&ctl->next[phase], 1ull);
+  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&ctl->next[phase], 1ull) + nw;
   return __shfl_sync(0xffffffffu, c, 0);
 }
 
@@ -349,6 +354,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   const int G = P.G;
   const int lr = blockIdx.x / G;
   const uint32_t wid = (blockIdx.x % G) * kWarps + (threadIdx.x >> 5);
+  const uint32_t NW = (uint32_t)G * kWarps;  // this rank's warps in this launch
   const RankCtx& R = P.rk[lr];
   const int p = P.p, r = R.rank, succ = (r + 1) % p;
   Ctl* ctl = reinterpret_cast<Ctl*>(R.inbox + P.L.off_ctl);
@@ -358,6 +364,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   const bool slot_mode = R.slot != nullptr;
   int bad = 0;
   stamp(P, wid, lr, 0);
+  // an earlier call failed on some rank: this one ends at once, reported as
+  // a consequence of the peer's failure (no timeout wait)
+  if (aborted(P, ctl)) {
+    if (wid == 0 && lane_id() == 0) latch_error(err, kErrTimeout, kPhRS, 0, -1, r, 1);
+    return;
+  }
 
   // Local pre-compress fused into every load of x (engine.py:333, :355/:400:
   // the ring input is D(C(grad)) under the whole-vector codec). For quant8
@@ -387,7 +399,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   auto give_up = [&]() -> bool {
     if (ll_fail) return true;
     if (aborted(P, ctl)) {
-      ll_fail = 2;
+      ll_fail = abort_detail(ctl, r) == 0 ? 3 : 2;  // 3: this rank's own abort (same missing peer)
       return true;
     }
     const uint64_t now = globaltimer();
@@ -407,10 +419,11 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   };
   // warp: any lane gave up -> latch like warp_await and leave
   auto ll_ok = [&](int phase, int step, int block) -> bool {
-    const int any = __any_sync(0xffffffffu, ll_fail != 0), own = __any_sync(0xffffffffu, ll_fail == 1);
+    const int any = __any_sync(0xffffffffu, ll_fail != 0), own = __any_sync(0xffffffffu, ll_fail == 1),
+              mine = __any_sync(0xffffffffu, ll_fail == 3);
     if (!any) return true;
     if (lane_id() == 0) {
-      latch_error(err, kErrTimeout, phase, step, block, r, own ? 0 : 1);
+      latch_error(err, kErrTimeout, phase, step, block, r, (own || mine) ? 0 : 1);
       if (own) broadcast_abort(P, R);
     }
     return false;
@@ -435,56 +448,28 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     return ok && ll_ok(phase, step, block);
   };
 
-  // ---- reduce-scatter step 0, send side: C(x_r[block r]) -> succ slot 0
-  {
-    const Blk B = get_blk(P, r);
-    Q8 q = q8_make(0.f);
-    if constexpr (C == kQuant8) {
-      float vmax;
-      if (!P.pre) {
-        uint32_t m = 0;
-        for (uint32_t c = grab(ctl, 0); c < B.nch; c = grab(ctl, 0))
-          for_groups<C>(P, B, c,
-                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
-                        [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
-        if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
-      } else {
-        // one pass over the whole local vector: max|x| (pre-compress scale)
-        // and max|x| over the own block, whose D(C(.)) maximum is
-        // D(C(max|x_r|)) because encode/decode are monotone in |x|
-        Blk W;
-        W.start = 0; W.len = P.n; W.A = 0;
-        W.nch = P.n ? (uint32_t)((P.n + P.chunk - 1) / P.chunk) : 0u;
-        uint32_t m = 0, mo = 0;
-        for (uint32_t c = grab(ctl, 0); c < W.nch; c = grab(ctl, 0))
-          for_groups<C>(P, W, c,
-                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
-                        [&](uint64_t g0, uint64_t, uint64_t, int, int, const FV<E>& v) {
-                          m = max(m, absmax_bits(v));
-#pragma unroll
-                          for (int i = 0; i < E; ++i) {
-                            const uint64_t g = g0 + i;
-                            if (g >= B.start && g < B.start + B.len) mo = max(mo, __float_as_uint(v.v[i]) & 0x7FFFFFFFu);
-                          }
-                        });
-        // own-block maximum goes through a second max slot before the
-        // barrier arrival so it is complete when the barrier opens
-        const uint32_t mow = warp_max_u32(mo);
-        if (lane_id() == 0) atomicMax(&ctl->maxslot[8], ((unsigned long long)s_seq << 32) | mow);
-        float xmax;
-        if (!warp_barrier_max(P, R, ctl, err, 0, m, xmax, 0)) return;
-        const float own = read_max_slot(ctl, 8);
-        if (nonfinite(xmax)) bad = 1;  // reference compress() rejects the whole local vector
-        q0 = q8_make(q8_scale(xmax));
-        vmax = fabsf(q8_decode(q8_encode(own, q0), q0.s));
-      }
-      q = q8_make(q8_scale(vmax));
-      stamp(P, wid, lr, 16);
-    }
-    uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
-    uint8_t* lld = ll_ptr(R.peer[succ], P.L, rs_slot(0));
-    bool first0 = true;
-    for (uint32_t c = grab(ctl, 1); c < B.nch; c = grab(ctl, 1)) {
+  // ---- codec none, p >= 3: direct reduce-scatter over NVSwitch. The ring's
+  // p-1 dependent hops become one: every rank pushes each block it does not
+  // own straight to the block's owner (slot d = its fold position), and the
+  // owner folds s_0 = x_b, s_k = fl(x_{b+k} + s_{k-1}) over the slots in the
+  // reference's order (collective.py:99-115; D(C(.)) is the identity for
+  // codec none, so the bits are the ring's). Same wire bytes per rank.
+  const bool own_via_inbox = slot_mode && C == kQuant8;  // owner re-quantises later, with the global scale
+  auto direct_rs = [&]() -> bool {
+    const int own = (r + 1) % p;
+    uint32_t NCH = 0;
+    for (int b = 0; b < p; ++b) NCH = max(NCH, get_blk(P, b).nch);
+    const Q8 q = q8_make(0.f);
+    // send: block b = (r - d) % p goes to its owner (b - 1) % p, slot d
+    for (uint32_t j = wid; j < (uint32_t)(p - 1) * NCH; j = grab(ctl, 1, NW)) {
+      const int d = (int)(j / NCH);
+      const uint32_t c = j % NCH;
+      const int b = (r - d + p) % p;
+      const Blk B = get_blk(P, b);
+      if (c >= B.nch) continue;
+      const int o = (b - 1 + p) % p;
+      uint8_t* dst = slot_ptr(R.peer[o], P.L, rs_slot(d));
+      uint8_t* lld = ll_ptr(R.peer[o], P.L, rs_slot(d));
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
@@ -492,138 +477,289 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                       if (ll) ll_put(ll_line<C>(lld, g0 - B.A), pk);
                       else store_pay<C>(dst, g0 - B.A, vlo, vhi, pk);
                     });
-      stamp2(P, wid, lr, 7, first0);
-      if (ll) ll_hdr_put(lld, c, r, B.len, q.s);
-      else warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
-      stamp2(P, wid, lr, 8, first0);
-      first0 = false;
+      if (ll) ll_hdr_put(lld, c, b, B.len, 0.f);
+      else warp_publish(P, R.peer[o], rs_slot(d), c, b, B.len, 0.f);
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhRS, 0, r, r, 0);
     bad = 0;
     stamp(P, wid, lr, 1);
-  }
-
-  // ---- reduce-scatter steps: fold block (r-s-1)%p, forward (or own it)
-  const bool own_via_inbox = slot_mode && C == kQuant8;  // owner re-quantises later, with the global scale
-  for (int s = 0; s < p - 1; ++s) {
-    const int b = (r - s - 1 + p) % p;
-    const Blk B = get_blk(P, b);
-    const bool last = (s == p - 2);
-    const uint8_t* in_slot = slot_ptr(R.inbox, P.L, rs_slot(s));
-    uint8_t* fwd = last ? nullptr : slot_ptr(R.peer[succ], P.L, rs_slot(s + 1));
-    const uint8_t* ll_in = ll_ptr(R.inbox, P.L, rs_slot(s));
-    uint8_t* ll_fwd = last ? nullptr : ll_ptr(R.peer[succ], P.L, rs_slot(s + 1));
-    auto load_xin = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
-      return XIn<E>{load_fv<E>(x, g0, lo, hi), ll ? ll_load(ll_in, g0 - B.A) : load_pay<C>(in_slot, g0 - B.A, vlo, vhi)};
-    };
-    auto emit = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const uint4& pk, float sc) {
-      if (!last) {
-        if (ll) ll_put(ll_line<C>(ll_fwd, g0 - B.A), pk);
-        else store_pay<C>(fwd, g0 - B.A, vlo, vhi, pk);
-      } else {
-        for (int d = 1; d < p; ++d) {
-          if (ll) ll_put(ll_line<C>(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A), pk);
-          else store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
-        }
-        if (own_via_inbox) {
-          if (ll) ll_put(ll_line<C>(ll_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A), pk);
-          else store_pay<C>(slot_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
-        } else if (slot_mode)
-          store_pay<C>(R.slot, g0, vlo, vhi, pk);  // none/trunc16: C(D(wire)) == wire
-        else
-          store_fv<E>(out, g0, lo, hi, decode_v<C>(pk, sc));
-      }
-    };
-    auto publish_last = [&](uint32_t c, float sc) {
+    // fold the owned block over slots 0 .. p-2 and the own x, then push the
+    // result to every peer's allgather slot (the ring's last hop)
+    const Blk B = get_blk(P, own);
+    constexpr int U = LL ? 1 : 2;  // groups per lane per batch: U x p loads in flight
+    bool first = true;
+    for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2, NW)) {
       if (ll) {
-        for (int d = 1; d < p; ++d) ll_hdr_put(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), c, b, B.len, sc);
-        if (own_via_inbox) ll_hdr_put(ll_ptr(R.inbox, P.L, ag_slot(p, b)), c, b, B.len, sc);
-        return;
-      }
-      warp_publish_all(P, R, b, c, B.len, sc);
-      if (own_via_inbox && lane_id() == 0) {
-        if (c == 0) write_hdr(P, R.inbox, ag_slot(p, b), b, B.len, sc);
-        st_release_sys(flag_ptr(R.inbox, P.L, ag_slot(p, b), c), flag_word(sc));
-      }
-    };
-
-    if constexpr (C != kQuant8) {
-      const Q8 q = q8_make(0.f);
-      bool first = true;
-      for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
-        float sin = 0.f;
-        stamp2(P, wid, lr, 4, first);
-        if (ll) {
-          if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
-        } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
-          return;
+        float sdum;
+        for (int d = 0; d < p - 1; ++d)
+          if (!ll_hdr_get(ll_ptr(R.inbox, P.L, rs_slot(d)), c, kPhRS, d, own, B.len, sdum)) return false;
+      } else {
+        // lane d waits for slot d's chunk flag (p - 1 waits in parallel)
+        int ok = 1;
+        const int d = lane_id();
+        if (d < p - 1) {
+          const uint64_t v = spin_flag(flag_ptr(R.inbox, P.L, rs_slot(d), c), P, R, ctl, err, kPhRS, d, own);
+          ok = v != 0;
+          if (ok && c == 0) {
+            const SlotHdr* h = hdr_ptr(R.inbox, P.L, rs_slot(d));
+            const uint32_t hb = __ldcg(&h->block), hi = __ldcg(&h->iteration), hn = __ldcg(&h->n_elems);
+            if (hb != (uint32_t)own || hi != P.iteration || hn != (uint32_t)B.len) {
+              latch_error(err, kErrHeader, kPhRS, d, own, r, (int)hn);
+              broadcast_abort(P, R);
+              ok = 0;
+            }
+          }
         }
-        if (first) stamp(P, wid, lr, 2 + 2 * s);
-        for_groups<C>(P, B, c, load_xin,
-                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
-                        emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
-                             0.f);
-                      });
-        if (ll && !ll_ok(kPhRS, s, b)) return;
-        stamp2(P, wid, lr, 5, first);
-        if (!last) {
-          if (ll) ll_hdr_put(ll_fwd, c, b, B.len, 0.f);
-          else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
-        } else {
-          publish_last(c, 0.f);
-        }
-        stamp2(P, wid, lr, 6, first);
-        first = false;
+        if (!__all_sync(0xffffffffu, ok)) return false;
       }
-    } else {
-      // pass A: fold into `out` (scratch for this block) and reduce the max
-      uint32_t m = 0;
-      bool first = true;
-      for (uint32_t c = grab(ctl, 2 + 2 * s); c < B.nch; c = grab(ctl, 2 + 2 * s)) {
-        float sin;
-        if (ll) {
-          if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
-        } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
-          return;
+      if (first) stamp(P, wid, lr, 2);
+      first = false;
+      const uint64_t cbase = B.A + (uint64_t)c * P.chunk;
+      const uint64_t lo = max(B.start, cbase), hi = min(B.start + B.len, cbase + P.chunk);
+      for (uint64_t b0 = cbase; b0 < hi; b0 += 32ull * E * U) {
+        uint4 in[U][kMaxRanks - 1];
+        FV<E> xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t g0 = b0 + (uint64_t)(u * 32 + lane_id()) * E;
+          if (g0 < hi && g0 + E > lo) {
+            const int vlo = (int)(max(lo, g0) - g0), vhi = (int)(min(hi, g0 + E) - g0);
+            xv[u] = load_fv<E>(x, g0, lo, hi);
+#pragma unroll
+            for (int d = 0; d < kMaxRanks - 1; ++d)
+              if (d < p - 1)
+                in[u][d] = ll ? ll_load(ll_ptr(R.inbox, P.L, rs_slot(d)), g0 - B.A)
+                              : load_pay<C>(slot_ptr(R.inbox, P.L, rs_slot(d)), g0 - B.A, vlo, vhi);
+          }
         }
-        if (first) stamp(P, wid, lr, 2 + 2 * s);
-        first = false;
-        for_groups<C>(P, B, c, load_xin,
-                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
-                        const FV<E> acc = add_v(px(v.x), decode_v<C>(v.in, sin));
-                        m = max(m, absmax_bits(acc));
-                        store_fv<E>(out, g0, lo, hi, acc);
-                      });
-        if (ll && !ll_ok(kPhRS, s, b)) return;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t g0 = b0 + (uint64_t)(u * 32 + lane_id()) * E;
+          if (!(g0 < hi && g0 + E > lo)) continue;
+          const int vlo = (int)(max(lo, g0) - g0), vhi = (int)(min(hi, g0 + E) - g0);
+          FV<E> acc = decode_v<C>(in[u][0], 0.f);  // s_0 = x_b
+#pragma unroll
+          for (int d = 1; d < kMaxRanks - 1; ++d)
+            if (d < p - 1) {
+              (void)encode_v<C>(acc, q, bad);  // the reference compresses s_{d-1} (finite check)
+              acc = add_v(decode_v<C>(in[u][d], 0.f), acc);
+            }
+          (void)encode_v<C>(acc, q, bad);
+          acc = add_v(px(xv[u]), acc);  // s_{p-1} = x_own + s_{p-2}
+          const uint4 pk = encode_v<C>(acc, q, bad);
+          for (int k = 1; k < p; ++k) {
+            if (ll) ll_put(ll_line<C>(ll_ptr(R.peer[(r + k) % p], P.L, ag_slot(p, own)), g0 - B.A), pk);
+            else store_pay<C>(slot_ptr(R.peer[(r + k) % p], P.L, ag_slot(p, own)), g0 - B.A, vlo, vhi, pk);
+          }
+          if (slot_mode) store_pay<C>(R.slot, g0, vlo, vhi, pk);
+          else store_fv<E>(out, g0, lo, hi, acc);
+        }
       }
-      float vmax;
-      if (s == 0) stamp(P, wid, lr, 15);  // (p = 2: slot 15 is free) pass A done
-      if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
-      if (s == 0) stamp(P, wid, lr, 17);
-      const Q8 q = q8_make(q8_scale(vmax));
-      // pass B: encode the partial with the block scale and push it (any
-      // warp may take any chunk: pass A's partials are visible GPU-wide
-      // after the barrier and are read through L2)
-      for (uint32_t c = grab(ctl, 3 + 2 * s); c < B.nch; c = grab(ctl, 3 + 2 * s)) {
-        for_groups<C>(P, B, c,
-                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
-                        return load_fv<E, false>(out, g0, lo, hi);
-                      },
-                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const FV<E>& acc) {
-                        emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
-                      });
-        if (!last) {
-          if (ll) ll_hdr_put(ll_fwd, c, b, B.len, q.s);
-          else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
-        } else {
-          publish_last(c, q.s);
-        }
+      if (ll && !ll_ok(kPhRS, p - 2, own)) return false;
+      if (ll) {
+        for (int k = 1; k < p; ++k) ll_hdr_put(ll_ptr(R.peer[(r + k) % p], P.L, ag_slot(p, own)), c, own, B.len, 0.f);
+      } else {
+        warp_publish_all(P, R, own, c, B.len, 0.f);
       }
     }
-    if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
-      latch_error(err, kErrNonFinite, last ? kPhAG : kPhRS, last ? 0 : s + 1, b, r, 0);
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhAG, 0, own, r, 0);
     bad = 0;
-    stamp(P, wid, lr, 3 + 2 * s);
+    stamp(P, wid, lr, 3);
+    return true;
+  };
+
+  if (C == kNone && P.direct) {
+    if (!direct_rs()) return;
+  } else {
+    // ---- reduce-scatter step 0, send side: C(x_r[block r]) -> succ slot 0
+    {
+      const Blk B = get_blk(P, r);
+      Q8 q = q8_make(0.f);
+      if constexpr (C == kQuant8) {
+        float vmax;
+        if (!P.pre) {
+          uint32_t m = 0;
+          for (uint32_t c = wid; c < B.nch; c = grab(ctl, 0, NW))
+            for_groups<C>(P, B, c,
+                          [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                          [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
+          if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
+        } else {
+          // one pass over the whole local vector: max|x| (pre-compress scale)
+          // and max|x| over the own block, whose D(C(.)) maximum is
+          // D(C(max|x_r|)) because encode/decode are monotone in |x|
+          Blk W;
+          W.start = 0; W.len = P.n; W.A = 0;
+          W.nch = P.n ? (uint32_t)((P.n + P.chunk - 1) / P.chunk) : 0u;
+          uint32_t m = 0, mo = 0;
+          for (uint32_t c = wid; c < W.nch; c = grab(ctl, 0, NW))
+            for_groups<C>(P, W, c,
+                          [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                          [&](uint64_t g0, uint64_t, uint64_t, int, int, const FV<E>& v) {
+                            m = max(m, absmax_bits(v));
+  #pragma unroll
+                            for (int i = 0; i < E; ++i) {
+                              const uint64_t g = g0 + i;
+                              if (g >= B.start && g < B.start + B.len) mo = max(mo, __float_as_uint(v.v[i]) & 0x7FFFFFFFu);
+                            }
+                          });
+          // own-block maximum goes through a second max slot before the
+          // barrier arrival so it is complete when the barrier opens
+          const uint32_t mow = warp_max_u32(mo);
+          if (lane_id() == 0) atomicMax(&ctl->maxslot[8], ((unsigned long long)s_seq << 32) | mow);
+          float xmax;
+          if (!warp_barrier_max(P, R, ctl, err, 0, m, xmax, 0)) return;
+          const float own = read_max_slot(ctl, 8);
+          if (nonfinite(xmax)) bad = 1;  // reference compress() rejects the whole local vector
+          q0 = q8_make(q8_scale(xmax));
+          vmax = fabsf(q8_decode(q8_encode(own, q0), q0.s));
+        }
+        q = q8_make(q8_scale(vmax));
+        stamp(P, wid, lr, 16);
+      }
+      uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
+      uint8_t* lld = ll_ptr(R.peer[succ], P.L, rs_slot(0));
+      bool first0 = true;
+      for (uint32_t c = wid; c < B.nch; c = grab(ctl, 1, NW)) {
+        for_groups<C>(P, B, c,
+                      [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                      [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
+                        const uint4 pk = encode_v<C>(px(v), q, bad);
+                        if (ll) ll_put(ll_line<C>(lld, g0 - B.A), pk);
+                        else store_pay<C>(dst, g0 - B.A, vlo, vhi, pk);
+                      });
+        stamp2(P, wid, lr, 7, first0);
+        if (ll) ll_hdr_put(lld, c, r, B.len, q.s);
+        else warp_publish(P, R.peer[succ], rs_slot(0), c, r, B.len, q.s);
+        stamp2(P, wid, lr, 8, first0);
+        first0 = false;
+      }
+      if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhRS, 0, r, r, 0);
+      bad = 0;
+      stamp(P, wid, lr, 1);
+    }
+
+    // ---- reduce-scatter steps: fold block (r-s-1)%p, forward (or own it)
+    for (int s = 0; s < p - 1; ++s) {
+      const int b = (r - s - 1 + p) % p;
+      const Blk B = get_blk(P, b);
+      const bool last = (s == p - 2);
+      const uint8_t* in_slot = slot_ptr(R.inbox, P.L, rs_slot(s));
+      uint8_t* fwd = last ? nullptr : slot_ptr(R.peer[succ], P.L, rs_slot(s + 1));
+      const uint8_t* ll_in = ll_ptr(R.inbox, P.L, rs_slot(s));
+      uint8_t* ll_fwd = last ? nullptr : ll_ptr(R.peer[succ], P.L, rs_slot(s + 1));
+      auto load_xin = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
+        return XIn<E>{load_fv<E>(x, g0, lo, hi), ll ? ll_load(ll_in, g0 - B.A) : load_pay<C>(in_slot, g0 - B.A, vlo, vhi)};
+      };
+      auto emit = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const uint4& pk, float sc) {
+        if (!last) {
+          if (ll) ll_put(ll_line<C>(ll_fwd, g0 - B.A), pk);
+          else store_pay<C>(fwd, g0 - B.A, vlo, vhi, pk);
+        } else {
+          for (int d = 1; d < p; ++d) {
+            if (ll) ll_put(ll_line<C>(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A), pk);
+            else store_pay<C>(slot_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+          }
+          if (own_via_inbox) {
+            if (ll) ll_put(ll_line<C>(ll_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A), pk);
+            else store_pay<C>(slot_ptr(R.inbox, P.L, ag_slot(p, b)), g0 - B.A, vlo, vhi, pk);
+          } else if (slot_mode)
+            store_pay<C>(R.slot, g0, vlo, vhi, pk);  // none/trunc16: C(D(wire)) == wire
+          else
+            store_fv<E>(out, g0, lo, hi, decode_v<C>(pk, sc));
+        }
+      };
+      auto publish_last = [&](uint32_t c, float sc) {
+        if (ll) {
+          for (int d = 1; d < p; ++d) ll_hdr_put(ll_ptr(R.peer[(r + d) % p], P.L, ag_slot(p, b)), c, b, B.len, sc);
+          if (own_via_inbox) ll_hdr_put(ll_ptr(R.inbox, P.L, ag_slot(p, b)), c, b, B.len, sc);
+          return;
+        }
+        warp_publish_all(P, R, b, c, B.len, sc);
+        if (own_via_inbox && lane_id() == 0) {
+          if (c == 0) write_hdr(P, R.inbox, ag_slot(p, b), b, B.len, sc);
+          st_release_sys(flag_ptr(R.inbox, P.L, ag_slot(p, b), c), flag_word(sc));
+        }
+      };
+
+      if constexpr (C != kQuant8) {
+        const Q8 q = q8_make(0.f);
+        bool first = true;
+        for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2 + 2 * s, NW)) {
+          float sin = 0.f;
+          stamp2(P, wid, lr, 4, first);
+          if (ll) {
+            if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
+          } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
+            return;
+          }
+          if (first) stamp(P, wid, lr, 2 + 2 * s);
+          for_groups<C>(P, B, c, load_xin,
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
+                          emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
+                               0.f);
+                        });
+          if (ll && !ll_ok(kPhRS, s, b)) return;
+          stamp2(P, wid, lr, 5, first);
+          if (!last) {
+            if (ll) ll_hdr_put(ll_fwd, c, b, B.len, 0.f);
+            else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, 0.f);
+          } else {
+            publish_last(c, 0.f);
+          }
+          stamp2(P, wid, lr, 6, first);
+          first = false;
+        }
+      } else {
+        // pass A: fold into `out` (scratch for this block) and reduce the max
+        uint32_t m = 0;
+        bool first = true;
+        for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2 + 2 * s, NW)) {
+          float sin;
+          if (ll) {
+            if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
+          } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
+            return;
+          }
+          if (first) stamp(P, wid, lr, 2 + 2 * s);
+          first = false;
+          for_groups<C>(P, B, c, load_xin,
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
+                          const FV<E> acc = add_v(px(v.x), decode_v<C>(v.in, sin));
+                          m = max(m, absmax_bits(acc));
+                          store_fv<E>(out, g0, lo, hi, acc);
+                        });
+          if (ll && !ll_ok(kPhRS, s, b)) return;
+        }
+        float vmax;
+        if (s == 0) stamp(P, wid, lr, 15);  // (p = 2: slot 15 is free) pass A done
+        if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
+        if (s == 0) stamp(P, wid, lr, 17);
+        const Q8 q = q8_make(q8_scale(vmax));
+        // pass B: encode the partial with the block scale and push it (any
+        // warp may take any chunk: pass A's partials are visible GPU-wide
+        // after the barrier and are read through L2)
+        for (uint32_t c = wid; c < B.nch; c = grab(ctl, 3 + 2 * s, NW)) {
+          for_groups<C>(P, B, c,
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
+                          return load_fv<E, false>(out, g0, lo, hi);
+                        },
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const FV<E>& acc) {
+                          emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
+                        });
+          if (!last) {
+            if (ll) ll_hdr_put(ll_fwd, c, b, B.len, q.s);
+            else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
+          } else {
+            publish_last(c, q.s);
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
+        latch_error(err, kErrNonFinite, last ? kPhAG : kPhRS, last ? 0 : s + 1, b, r, 0);
+      bad = 0;
+      stamp(P, wid, lr, 3 + 2 * s);
+    }
   }
 
   // ---- slot mode, quant8: the pipe re-compress (engine.py:407) needs the
@@ -671,7 +807,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const uint8_t* in_slot = slot_ptr(R.inbox, P.L, ag_slot(p, b));
     const uint8_t* ll_in = ll_ptr(R.inbox, P.L, ag_slot(p, b));
     bool first = true;
-    for (uint32_t c = grab(ctl, 20 + k); c < B.nch; c = grab(ctl, 20 + k)) {
+    for (uint32_t c = wid; c < B.nch; c = grab(ctl, 20 + k, NW)) {
       float sin = 0.f;
       stamp2(P, wid, lr, 9, first && k == 1);
       if (ll) {

@@ -51,13 +51,42 @@ struct Layout {
 
 struct Ctl {                   // rank-private control block (peers write abort / ack)
   unsigned long long bar;      // quant8 barrier arrivals in the current call
-  unsigned long long abort;    // == seq when the current call aborted
+  unsigned long long abort;    // kAbortSticky | seq of the call that failed (0 = healthy)
   unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier (reset per call)
   unsigned long long calls;    // sequence number of the last completed call
   unsigned long long exits;    // warps that finished the current call
   unsigned long long next[32]; // per-phase chunk counters (dynamic chunk scheduling)
   unsigned long long ack[kMaxRanks];  // star calls: == seq once rank q consumed this rank's data
 };
+
+// A failed call (timeout, header mismatch) poisons the communicator on every
+// rank: the abort word keeps bit 63 set, so every later call -- not only the
+// one that failed -- stops at once instead of waiting out its own timeout
+// (the reference's run ends at the first failed recv, collective.py:157-161;
+// the Python endpoint is unusable after a CollectiveError). Bits [39:32] hold
+// the aborting rank + 1: a warp that sees its own rank's abort was waiting
+// for the same missing peer (its own timeout), not for a failed peer.
+constexpr unsigned long long kAbortSticky = 1ull << 63;
+
+__device__ __forceinline__ unsigned long long abort_word(const Ctl* ctl) {
+  return *(const volatile unsigned long long*)&ctl->abort;
+}
+__device__ __forceinline__ bool comm_aborted(const Ctl* ctl) { return (abort_word(ctl) & kAbortSticky) != 0; }
+// detail of the error a warp latches when it stops on an abort: 0 = this
+// rank's own timeout (another warp of the rank gave up first), 1 = a peer failed
+__device__ __forceinline__ int abort_detail(const Ctl* ctl, int rank) {
+  return (int)((abort_word(ctl) >> 32) & 0xFF) == rank + 1 ? 0 : 1;
+}
+
+// Poison this communicator on every rank (peers' ctl blocks over NVLink).
+__device__ __forceinline__ void abort_all(uint8_t* const* peer, int p, uint64_t off_ctl, uint32_t seq, int rank) {
+  const unsigned long long w = kAbortSticky | ((unsigned long long)((rank + 1) & 0xFF) << 32) | seq;
+  for (int q = 0; q < p; ++q) {
+    Ctl* c = reinterpret_cast<Ctl*>(peer[q] + off_ctl);
+    atomicCAS(&c->abort, 0ull, w);  // the first abort names its rank
+  }
+  fence_sys();
+}
 
 // Call sequence numbers cycle through 1 .. 2^32 - 1: never 0 (the value of
 // zero-initialised flags and LL words), and every check compares for
@@ -93,6 +122,7 @@ struct RingParams {
   int p, codec, G;             // world size, codec tag, CTAs per rank (kRingWarps warp workers each)
   int pre;                     // x is the raw gradient: apply the local D(C(.)) on load
   int ll;                      // this call uses the LL protocol (see ll_payload_limit)
+  int direct;                  // codec none, p >= 3: direct reduce-scatter (one hop, ring.cu)
   unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
 
@@ -118,6 +148,7 @@ struct StarLaunch {
   Layout L;
   uint64_t n, timeout_ns;
   int p, root, mode, zero_first, ctas, nlocal;
+  int max_ctas;  // co-residency cap of one launch (SM count; emulated: all ranks' CTAs)
   const float* ins[kMaxRanks];
   float* outs[kMaxRanks];
   uint8_t* inboxes[kMaxRanks];

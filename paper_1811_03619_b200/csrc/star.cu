@@ -55,8 +55,8 @@ __device__ __forceinline__ float* staged(uint8_t* inbox, const Layout& L) {
   return reinterpret_cast<float*>(inbox + L.off_payload);
 }
 
-__device__ bool star_wait(const uint64_t* f, const StarParams& P, Ctl* ctl, ErrWord* err, int phase, int src,
-                          int rank) {
+__device__ bool star_wait(const uint64_t* f, const StarParams& P, const StarRank& R, Ctl* ctl, ErrWord* err,
+                          int phase, int src, int rank) {
   if ((uint32_t)(ld_acquire_sys(f) >> 32) == s_star_seq) return true;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 64;
@@ -68,12 +68,13 @@ __device__ bool star_wait(const uint64_t* f, const StarParams& P, Ctl* ctl, ErrW
     __nanosleep(ns);
     if (ns < 512) ns <<= 1;
     if ((it & 31u) == 0) {
-      if ((uint32_t)(*(volatile unsigned long long*)&ctl->abort) == s_star_seq) {
-        latch_error(err, kErrTimeout, phase, 0, src, rank, 1);
+      if (comm_aborted(ctl)) {
+        latch_error(err, kErrTimeout, phase, 0, src, rank, abort_detail(ctl, rank));
         return false;
       }
       if (globaltimer() - t0 > P.timeout_ns) {
         latch_error(err, kErrTimeout, phase, 0, src, rank, 0);
+        abort_all(R.peer, P.p, P.L.off_ctl, s_star_seq, rank);  // peers stop waiting on this rank
         return false;
       }
     }
@@ -124,6 +125,10 @@ __device__ void star_body(const StarParams& P) {
   const int slot = P.mode;  // flags: slot 0 gather staging, slot 1 broadcast staging
   const int phase = P.mode == 0 ? kPhRS : kPhAG;
   const bool root = R.rank == P.root;
+  if (comm_aborted(ctl)) {  // an earlier call failed: end at once (ring.cuh:kAbortSticky)
+    if (blockIdx.x % P.G == 0 && threadIdx.x == 0) latch_error(err, kErrTimeout, phase, 0, -1, R.rank, 1);
+    return;
+  }
 
   if ((P.mode == 0 && !root) || (P.mode == 1 && root)) {
     // stage my vector in my inbox and publish it chunk by chunk
@@ -142,7 +147,7 @@ __device__ void star_body(const StarParams& P) {
     const float* src = staged(R.peer[P.root], P.L);
     for (uint32_t c = star_grab(ctl, 1); c < nch; c = star_grab(ctl, 1)) {
       int ok = 1;
-      if (lane == 0) ok = star_wait(star_flag(R.peer[P.root], P.L, slot, c), P, ctl, err, phase, P.root, R.rank);
+      if (lane == 0) ok = star_wait(star_flag(R.peer[P.root], P.L, slot, c), P, R, ctl, err, phase, P.root, R.rank);
       __syncwarp();
       if (!__shfl_sync(0xffffffffu, ok, 0)) return;
       const uint64_t b = (uint64_t)c * P.chunk, e = min(n, b + P.chunk);
@@ -157,7 +162,7 @@ __device__ void star_body(const StarParams& P) {
     int ok = 1;
     if (lane == 0)
       for (int s = 0; s < P.p && ok; ++s)
-        if (s != R.rank) ok = star_wait(star_flag(R.peer[s], P.L, 0, c), P, ctl, err, phase, s, R.rank);
+        if (s != R.rank) ok = star_wait(star_flag(R.peer[s], P.L, 0, c), P, R, ctl, err, phase, s, R.rank);
     __syncwarp();
     if (!__shfl_sync(0xffffffffu, ok, 0)) return;
     const uint64_t b = (uint64_t)c * P.chunk, e = min(n, b + P.chunk);
@@ -213,9 +218,9 @@ __device__ void star_body(const StarParams& P) {
 }
 
 // Lane 0: wait until ack word `a` carries this call's sequence.
-__device__ bool star_wait_ack(unsigned long long* a, const StarParams& P, Ctl* ctl, ErrWord* err, int phase,
-                              int src, int rank) {
-  return star_wait(reinterpret_cast<const uint64_t*>(a), P, ctl, err, phase, src, rank);
+__device__ bool star_wait_ack(unsigned long long* a, const StarParams& P, const StarRank& R, Ctl* ctl, ErrWord* err,
+                              int phase, int src, int rank) {
+  return star_wait(reinterpret_cast<const uint64_t*>(a), P, R, ctl, err, phase, src, rank);
 }
 
 // Close of a star call, run by the last warp of a rank: the side whose
@@ -236,7 +241,7 @@ __device__ void star_close_handshake(const StarParams& P, const StarRank& R, Ctl
       for (int q = 0; q < P.p; ++q)
         if (q != R.rank) st_release_sys(reinterpret_cast<uint64_t*>(&peer_ctl(q)->ack[R.rank]), ackw);
     } else {
-      star_wait_ack(&ctl->ack[P.root], P, ctl, err, phase, P.root, R.rank);
+      star_wait_ack(&ctl->ack[P.root], P, R, ctl, err, phase, P.root, R.rank);
     }
   } else {
     if (!root) {
@@ -244,7 +249,7 @@ __device__ void star_close_handshake(const StarParams& P, const StarRank& R, Ctl
       st_release_sys(reinterpret_cast<uint64_t*>(&peer_ctl(P.root)->ack[R.rank]), ackw);
     } else {
       for (int q = 0; q < P.p; ++q)
-        if (q != R.rank && !star_wait_ack(&ctl->ack[q], P, ctl, err, phase, q, R.rank)) break;
+        if (q != R.rank && !star_wait_ack(&ctl->ack[q], P, R, ctl, err, phase, q, R.rank)) break;
     }
   }
 }
@@ -280,7 +285,7 @@ cudaError_t launch_star(const StarLaunch& S, cudaStream_t stream) {
   P.root = S.root;
   P.mode = S.mode;
   P.zero_first = S.zero_first;
-  P.G = std::max(1, std::min(S.ctas, 148));
+  P.G = std::max(1, std::min(S.ctas, S.max_ctas));
   // full-vector staging in the inbox payload, chunk flags sized per slot
   const uint64_t want = (S.n + S.L.max_chunks - 1) / std::max<uint64_t>(1, S.L.max_chunks);
   P.chunk = (uint32_t)std::max<uint64_t>(4096, (want + 1023) / 1024 * 1024);

@@ -192,6 +192,14 @@ class GpuTransport:
         self._comms = [_comm_create(r, world_size, devices[r], max_elems) for r in range(world_size)]
         for c in self._comms:
             _lib.call("gp_comm_set_tuning", c, int(ctas), float(timeout_s))
+        # chunk size, and so every flag index, follows the CTA budget G: all
+        # ranks must agree even when their devices' caps differ
+        g = min(ep_ctas(c) for c in self._comms)
+        for c in self._comms:
+            if ep_ctas(c) != g:
+                _lib.call("gp_comm_set_tuning", c, int(g), 0.0)
+        if len({ep_ctas(c) for c in self._comms}) != 1:
+            raise ConfigError("ranks disagree on the ring's CTA budget")
         if world_size > 1:
             arr = (ctypes.c_void_p * world_size)(*[c.value for c in self._comms])
             _lib.call("gp_comm_connect_local", arr, world_size)

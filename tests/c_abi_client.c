@@ -8,7 +8,7 @@
 #include "pipesgd.h"
 
 int main(void) {
-  int64_t plan[4];
+  int64_t plan[5];
   if (gp_version() != 1) return 1;
   /* C2 gradient over 2 ranks, trunc16, the standalone CTA budget */
   if (gp_ring_plan(4710538u, 2, 592, GP_CODEC_TRUNC16, 0, 4710538u, plan) != GP_OK) return 2;

@@ -88,9 +88,9 @@ def test_argument_errors_are_reported_without_a_gpu():
 
 def _plan(n, world, ctas, codec, flags=0, max_elems=None):
     from paper_1811_03619_b200 import _lib
-    out = (ctypes.c_int64 * 4)()
+    out = (ctypes.c_int64 * 5)()
     _lib.call("gp_ring_plan", n, world, ctas, codec, flags, max_elems or n, out)
-    return {"chunk": out[0], "ctas": out[1], "ll": out[2], "nch": out[3]}
+    return {"chunk": out[0], "ctas": out[1], "ll": out[2], "nch": out[3], "direct": out[4]}
 
 
 @pytest.mark.parametrize("world,codec", [(2, 0), (2, 1), (2, 2), (4, 0), (4, 1), (8, 0), (8, 2)])
@@ -107,7 +107,7 @@ def test_ll_protocol_threshold(world, codec):
 
 def test_launch_and_chunk_plan():
     # tiny calls launch one CTA; the chunk stays at its 1024-element minimum
-    assert _plan(8, 2, 592, 1) == {"chunk": 1024, "ctas": 1, "ll": 1, "nch": 1}
+    assert _plan(8, 2, 592, 1) == {"chunk": 1024, "ctas": 1, "ll": 1, "nch": 1, "direct": 0}
     # C2 gradient, standalone budget: 1024-element chunks, one per warp
     pl = _plan(4_710_538, 2, 592, 1)
     assert pl["chunk"] == 1024 and pl["nch"] == 2301 and pl["ctas"] == 576 and pl["ll"] == 0
@@ -117,6 +117,16 @@ def test_launch_and_chunk_plan():
     # quant8 with the fused pre-compress scans the whole vector in chunk units
     a, b = _plan(1_000_000, 4, 592, 2), _plan(1_000_000, 4, 592, 2, flags=1)
     assert b["nch"] >= 4 * a["nch"] - 4
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_direct_reduce_scatter_plan(world):
+    """codec none folds D(C(.)) = identity, so from 3 ranks on the owner folds
+    every rank's block after one hop (bit-identical to the ring's fold);
+    compressed codecs keep the ring (their partial sums travel compressed)."""
+    for codec in (0, 1, 2):
+        for n in (8, 1 << 20, 61_100_840):
+            assert _plan(n, world, 592, codec)["direct"] == int(codec == 0 and world >= 3)
 
 
 def test_plain_c_client_compiles_links_and_runs(tmp_path):

@@ -174,6 +174,25 @@ def test_p2p_timeout_produces_diagnostic(P):
 
 
 @multigpu
+def test_p2p_failure_poisons_every_later_call(P):
+    """After one rank timed out, the abort stays on every rank: a later call
+    on the healthy rank ends at once as a consequence of the peer's failure
+    instead of waiting out its own timeout (the reference's run ends at the
+    first failed recv, collective.py:157-161)."""
+    import time
+    tr = P.GpuTransport(2, timeout_s=1.0, max_elems=1 << 12)
+    try:
+        with pytest.raises(P.CollectiveError, match="timed out"):
+            P.ring_allreduce(np.ones(8, np.float32), 0, 2, tr.endpoint(0))
+        t0 = time.perf_counter()
+        with pytest.raises(P.CollectiveError, match="aborted after a peer failed"):
+            P.ring_allreduce(np.ones(8, np.float32), 1, 2, tr.endpoint(1))
+        assert time.perf_counter() - t0 < 0.5
+    finally:
+        tr.close()
+
+
+@multigpu
 @pytest.mark.parametrize("n", [300_007, 50_001])  # flag protocol / LL protocol (none, trunc16)
 def test_p2p_ring_in_cuda_graph_replays_bit_exact(P, n):
     """The call sequence number lives on the device, so one captured launch
