@@ -162,6 +162,48 @@ __device__ __forceinline__ FV<E> load_fv(const float* x, uint64_t g0, uint64_t l
   return r;
 }
 
+// L2 eviction-priority policies (createpolicy) for streams read twice: the
+// first read marks lines evict_last so the second read finds them in the
+// 126 MB L2; the second read marks them evict_first (their last use).
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ldg_hint(const float4* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ldcg_hint(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// load_fv of a read-only input with an L2 policy (edges take the plain path)
+template <int E>
+__device__ __forceinline__ FV<E> load_fv_pol(const float* x, uint64_t g0, uint64_t lo, uint64_t hi, uint64_t pol) {
+  if (!(lo <= g0 && g0 + E <= hi)) return load_fv<E>(x, g0, lo, hi);
+  FV<E> r;
+  const float4* p = reinterpret_cast<const float4*>(x + g0);
+#pragma unroll
+  for (int k = 0; k < E / 4; ++k) {
+    const float4 a = ldg_hint(p + k, pol);
+    r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
+  }
+  return r;
+}
+
 template <int E>
 __device__ __forceinline__ void store_fv(float* x, uint64_t g0, uint64_t lo, uint64_t hi, const FV<E>& r) {
   if (lo <= g0 && g0 + E <= hi) {
@@ -192,6 +234,13 @@ __device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, in
     w[(i * W) >> 2] |= e << bit;
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int C>
+__device__ __forceinline__ uint4 load_pay_pol(const uint8_t* slot, uint64_t rel0, int vlo, int vhi, uint64_t pol) {
+  constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
+  if (vlo == 0 && vhi == E) return ldcg_hint(reinterpret_cast<const uint4*>(slot + rel0 * W), pol);
+  return load_pay<C>(slot, rel0, vlo, vhi);
 }
 
 template <int C>

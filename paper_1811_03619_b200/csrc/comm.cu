@@ -362,6 +362,9 @@ int gp_comm_set_call_counter(gp_comm* c, uint64_t calls) {
     cudaError_t e = cudaMemcpy(c->inbox[i] + c->L.off_ctl + offsetof(Ctl, calls), &v, sizeof(v),
                                cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "set call counter");
+    // the next call's bank follows the counter's parity: start both from zero
+    e = cudaMemset(c->inbox[i] + c->L.off_ctl + offsetof(Ctl, bank), 0, sizeof(CtlBank) * 2);
+    if (e != cudaSuccess) return cuda_fail(e, "reset ctl banks");
   }
   return GP_OK;
 }

@@ -51,6 +51,11 @@ constexpr uint64_t kBatch = PIPESGD_RING_BATCH;  // elements per warp per batch 
 // It lives on the device (not in the launch parameters) so a launch can be
 // captured once in a CUDA graph and replayed: every replay is a new call.
 __shared__ uint32_t s_seq;
+__shared__ uint32_t s_bank;                 // ctl bank of this call (ring.cuh:CtlBank)
+__shared__ unsigned long long s_calls;      // raw count of calls completed before this one
+__shared__ unsigned long long s_abort;      // the abort word at kernel entry
+
+__device__ __forceinline__ CtlBank* cb(Ctl* c) { return &c->bank[s_bank]; }
 
 struct Blk {
   uint64_t start, len, A;
@@ -238,12 +243,12 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
   int ok = 1;
   float v = 0.f;
   if (lane_id() == 0) {
-    atomicMax(&ctl->maxslot[k], ((unsigned long long)s_seq << 32) | m);
+    atomicMax(&cb(ctl)->maxslot[k], ((unsigned long long)s_seq << 32) | m);
     __threadfence();
-    atomicAdd(&ctl->bar, 1ull);
+    atomicAdd(&cb(ctl)->bar, 1ull);
     const unsigned long long target = (unsigned long long)(k + 1) * P.G * kWarps;
     const uint64_t t0 = globaltimer();
-    for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->bar)) < target; ++it) {
+    for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->bar)) < target; ++it) {
       __nanosleep(64);
       if ((it & 63u) == 0) {
         if (aborted(P, ctl)) {
@@ -259,7 +264,7 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
         }
       }
     }
-    const unsigned long long w = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->maxslot[k]));
+    const unsigned long long w = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->maxslot[k]));
     v = ((uint32_t)(w >> 32) == s_seq) ? __uint_as_float((uint32_t)w) : 0.f;
   }
   __syncwarp();
@@ -324,7 +329,7 @@ __device__ __forceinline__ void stamp2(const RingParams& P, uint32_t wid, int lr
 // 3+2s quant8 push of step s, 20+k allgather of the k-th block.
 __device__ __forceinline__ uint32_t grab(Ctl* ctl, int phase, uint32_t nw) {
   uint32_t c = 0;
-  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&ctl->next[phase], 1ull) + nw;
+  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&cb(ctl)->next[phase], 1ull) + nw;
   return __shfl_sync(0xffffffffu, c, 0);
 }
 
@@ -340,7 +345,7 @@ struct XIn {
 __device__ __forceinline__ float read_max_slot(Ctl* ctl, int idx) {
   uint32_t w = 0;
   if (lane_id() == 0) {
-    const unsigned long long x = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->maxslot[idx]));
+    const unsigned long long x = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->maxslot[idx]));
     w = ((uint32_t)(x >> 32) == s_seq) ? (uint32_t)x : 0u;
   }
   return __uint_as_float(__shfl_sync(0xffffffffu, w, 0));
@@ -366,7 +371,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   stamp(P, wid, lr, 0);
   // an earlier call failed on some rank: this one ends at once, reported as
   // a consequence of the peer's failure (no timeout wait)
-  if (aborted(P, ctl)) {
+  if (s_abort & kAbortSticky) {
     if (wid == 0 && lane_id() == 0) latch_error(err, kErrTimeout, kPhRS, 0, -1, r, 1);
     return;
   }
@@ -579,9 +584,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         float vmax;
         if (!P.pre) {
           uint32_t m = 0;
+          const uint64_t keep = l2_evict_last();  // the send pass below re-reads the block
           for (uint32_t c = wid; c < B.nch; c = grab(ctl, 0, NW))
             for_groups<C>(P, B, c,
-                          [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
+                          [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
+                            return load_fv_pol<E>(x, g0, lo, hi, keep);
+                          },
                           [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
           if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
         } else {
@@ -606,7 +614,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           // own-block maximum goes through a second max slot before the
           // barrier arrival so it is complete when the barrier opens
           const uint32_t mow = warp_max_u32(mo);
-          if (lane_id() == 0) atomicMax(&ctl->maxslot[8], ((unsigned long long)s_seq << 32) | mow);
+          if (lane_id() == 0) atomicMax(&cb(ctl)->maxslot[8], ((unsigned long long)s_seq << 32) | mow);
           float xmax;
           if (!warp_barrier_max(P, R, ctl, err, 0, m, xmax, 0)) return;
           const float own = read_max_slot(ctl, 8);
@@ -711,7 +719,17 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           first = false;
         }
       } else {
-        // pass A: fold into `out` (scratch for this block) and reduce the max
+        // pass A: fold and reduce the block max. The partial sum is not
+        // stored: pass B recomputes it from the same x and inbox bytes (the
+        // same single fp32 add, so the same bits). pass A's loads mark their
+        // lines L2 evict_last, so when the hop's x block and inbox fit the
+        // 126 MB L2 (C3 at p >= 4: 61 + 15 MB) pass B re-reads them on chip
+        // instead of a 4 B/elem partial written to HBM and read back.
+        const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
+        auto load_xin_pol = [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, uint64_t pol) {
+          return XIn<E>{load_fv_pol<E>(x, g0, lo, hi, pol),
+                        ll ? ll_load(ll_in, g0 - B.A) : load_pay_pol<C>(in_slot, g0 - B.A, vlo, vhi, pol)};
+        };
         uint32_t m = 0;
         bool first = true;
         for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2 + 2 * s, NW)) {
@@ -723,11 +741,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           }
           if (first) stamp(P, wid, lr, 2 + 2 * s);
           first = false;
-          for_groups<C>(P, B, c, load_xin,
-                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int, const XIn<E>& v) {
-                          const FV<E> acc = add_v(px(v.x), decode_v<C>(v.in, sin));
-                          m = max(m, absmax_bits(acc));
-                          store_fv<E>(out, g0, lo, hi, acc);
+          for_groups<C>(P, B, c,
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
+                          return load_xin_pol(g0, lo, hi, vlo, vhi, keep);
+                        },
+                        [&](uint64_t, uint64_t, uint64_t, int, int, const XIn<E>& v) {
+                          m = max(m, absmax_bits(add_v(px(v.x), decode_v<C>(v.in, sin))));
                         });
           if (ll && !ll_ok(kPhRS, s, b)) return;
         }
@@ -736,17 +755,26 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
         if (s == 0) stamp(P, wid, lr, 17);
         const Q8 q = q8_make(q8_scale(vmax));
-        // pass B: encode the partial with the block scale and push it (any
-        // warp may take any chunk: pass A's partials are visible GPU-wide
-        // after the barrier and are read through L2)
+        // pass B: recompute the partial, encode it with the block scale and
+        // push it. Any warp may take any chunk: the chunk's flag (or LL
+        // lines) already carries this call's sequence, so the waits below
+        // return at once and hand this warp the chunk's incoming scale.
         for (uint32_t c = wid; c < B.nch; c = grab(ctl, 3 + 2 * s, NW)) {
+          float sin;
+          if (ll) {
+            if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
+          } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
+            return;
+          }
           for_groups<C>(P, B, c,
-                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
-                          return load_fv<E, false>(out, g0, lo, hi);
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
+                          return load_xin_pol(g0, lo, hi, vlo, vhi, drop);
                         },
-                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const FV<E>& acc) {
+                        [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
+                          const FV<E> acc = add_v(px(v.x), decode_v<C>(v.in, sin));
                           emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
                         });
+          if (ll && !ll_ok(kPhRS, s, b)) return;
           if (!last) {
             if (ll) ll_hdr_put(ll_fwd, c, b, B.len, q.s);
             else warp_publish(P, R.peer[succ], rs_slot(s + 1), c, b, B.len, q.s);
@@ -844,22 +872,29 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
-  if (threadIdx.x == 0) s_seq = next_seq(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)));
+  if (threadIdx.x == 0) {
+    const unsigned long long calls = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls));
+    s_calls = calls;
+    s_seq = next_seq(calls);
+    s_bank = (uint32_t)(calls & 1);
+    s_abort = *(volatile unsigned long long*)&ctl->abort;
+    if (blockIdx.x % P.G == 0) {  // the next call's bank starts from zero
+      CtlBank* nb = &ctl->bank[(calls + 1) & 1];
+      nb->bar = 0;
+      nb->exits = 0;
+      for (int i = 0; i < 32; ++i) nb->next[i] = 0;
+      for (int i = 0; i < 16; ++i) nb->maxslot[i] = 0;
+    }
+  }
   __syncthreads();
   ring_body<C, LL>(P);  // returns early (per warp) on timeout / abort / header mismatch
-  // Last warp of this rank to leave closes the call: counters reset, calls
-  // advanced. The next call on this stream starts only after this kernel.
+  // The last warp of this rank to leave closes the call by advancing the call
+  // count. The next call on this stream starts only after this kernel has
+  // completed, which also makes the bank zeroing above visible to it.
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
-    const unsigned long long prev = atomicAdd(&ctl->exits, 1ull);
-    if (prev == (unsigned long long)P.G * kWarps - 1) {
-      ctl->exits = 0;
-      ctl->bar = 0;
-      for (int i = 0; i < 32; ++i) ctl->next[i] = 0;
-      for (int i = 0; i < 16; ++i) ctl->maxslot[i] = 0;
-      __threadfence();
-      atomicExch(&ctl->calls, (unsigned long long)s_seq);
-    }
+    const unsigned long long prev = atomicAdd(&cb(ctl)->exits, 1ull);
+    if (prev == (unsigned long long)P.G * kWarps - 1) *(volatile unsigned long long*)&ctl->calls = s_calls + 1;
   }
 }
 

@@ -49,15 +49,23 @@ struct Layout {
   uint32_t nslot;        // 2p-1: p-1 reduce-scatter slots + p allgather slots
 };
 
+// Per-call scratch of the control block, double-banked: call k (k = the raw
+// count of completed calls) uses bank k & 1 and zeroes bank (k + 1) & 1 at its
+// start, so no call has to reset its counters (and fence) on the way out.
+struct CtlBank {
+  unsigned long long bar;          // quant8 barrier arrivals in the call
+  unsigned long long exits;        // warps that finished the call
+  unsigned long long next[32];     // per-phase chunk counters (dynamic chunk scheduling)
+  unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier
+};
+
 struct Ctl {                   // rank-private control block (peers write abort / ack)
-  unsigned long long bar;      // quant8 barrier arrivals in the current call
-  unsigned long long abort;    // kAbortSticky | seq of the call that failed (0 = healthy)
-  unsigned long long maxslot[16];  // (seq << 32) | absmax bits, per quant8 barrier (reset per call)
-  unsigned long long calls;    // sequence number of the last completed call
-  unsigned long long exits;    // warps that finished the current call
-  unsigned long long next[32]; // per-phase chunk counters (dynamic chunk scheduling)
+  unsigned long long calls;    // raw count of completed calls: seq = next_seq(calls)
+  unsigned long long abort;    // kAbortSticky | rank + 1 | seq of the call that failed (0 = healthy)
+  CtlBank bank[2];
   unsigned long long ack[kMaxRanks];  // star calls: == seq once rank q consumed this rank's data
 };
+static_assert(sizeof(Ctl) <= 2048, "ctl block: the p = 1 codec status lives at +2048");
 
 // A failed call (timeout, header mismatch) poisons the communicator on every
 // rank: the abort word keeps bit 63 set, so every later call -- not only the
@@ -90,8 +98,8 @@ __device__ __forceinline__ void abort_all(uint8_t* const* peer, int p, uint64_t 
 
 // Call sequence numbers cycle through 1 .. 2^32 - 1: never 0 (the value of
 // zero-initialised flags and LL words), and every check compares for
-// equality, so the 32-bit counter may wrap (a rank is never more than one
-// call ahead of the data it reads).
+// equality, so the 32-bit sequence may wrap (a rank is never more than one
+// call ahead of the data it reads). `calls` itself only counts up.
 __host__ __device__ inline uint32_t next_seq(unsigned long long calls) {
   return (uint32_t)(calls % 0xFFFFFFFFull) + 1u;
 }

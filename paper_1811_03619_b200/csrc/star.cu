@@ -28,6 +28,8 @@ constexpr int kStarThreads = 128;
 constexpr int kStarWarps = kStarThreads / 32;
 
 __shared__ uint32_t s_star_seq;
+__shared__ uint32_t s_star_bank;
+__shared__ unsigned long long s_star_calls;
 
 struct StarRank {
   const float* in;
@@ -83,7 +85,7 @@ __device__ bool star_wait(const uint64_t* f, const StarParams& P, const StarRank
 
 __device__ __forceinline__ uint32_t star_grab(Ctl* ctl, int phase) {
   uint32_t c = 0;
-  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&ctl->next[phase], 1ull);
+  if ((threadIdx.x & 31) == 0) c = (uint32_t)atomicAdd(&ctl->bank[s_star_bank].next[phase], 1ull);
   return __shfl_sync(0xffffffffu, c, 0);
 }
 
@@ -257,19 +259,28 @@ __device__ void star_close_handshake(const StarParams& P, const StarRank& R, Ctl
 __global__ void __launch_bounds__(kStarThreads) star_kernel(const __grid_constant__ StarParams P) {
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
-  if (threadIdx.x == 0) s_star_seq = next_seq(ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls)));
+  if (threadIdx.x == 0) {
+    const unsigned long long calls = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls));
+    s_star_calls = calls;
+    s_star_seq = next_seq(calls);
+    s_star_bank = (uint32_t)(calls & 1);
+    if (blockIdx.x % P.G == 0) {  // the next call's bank starts from zero (ring.cuh:CtlBank)
+      CtlBank* nb = &ctl->bank[(calls + 1) & 1];
+      nb->bar = 0;
+      nb->exits = 0;
+      for (int i = 0; i < 32; ++i) nb->next[i] = 0;
+      for (int i = 0; i < 16; ++i) nb->maxslot[i] = 0;
+    }
+  }
   __syncthreads();
   star_body(P);
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {  // last warp of this rank closes the call (as the ring does)
-    const unsigned long long prev = atomicAdd(&ctl->exits, 1ull);
+    const unsigned long long prev = atomicAdd(&ctl->bank[s_star_bank].exits, 1ull);
     if (prev == (unsigned long long)P.G * kStarWarps - 1) {
       __threadfence();  // every warp of this rank is done with the staged data
       star_close_handshake(P, P.rk[lr], ctl);
-      ctl->exits = 0;
-      for (int i = 0; i < 32; ++i) ctl->next[i] = 0;
-      __threadfence();
-      atomicExch(&ctl->calls, (unsigned long long)s_star_seq);
+      *(volatile unsigned long long*)&ctl->calls = s_star_calls + 1;
     }
   }
 }
