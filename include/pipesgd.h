@@ -92,12 +92,15 @@ int gp_comm_create(int rank, int world, int device, uint64_t max_elems, gp_comm*
 int gp_comm_create_emulated(int world, int device, uint64_t max_elems, gp_comm** out);
 int gp_comm_ipc_handle(gp_comm* comm, void* handle_out /* 64 bytes */);
 int gp_comm_connect_ipc(gp_comm* comm, const void* handles /* world x 64 bytes, rank order */);
+/* In-process peers (one thread per rank). Ranks may share a device: each keeps
+ * its own inbox and its own per-rank ring launch, and the device's SMs are split
+ * between them (every rank's CTA budget is capped so all launches co-reside). */
 int gp_comm_connect_local(gp_comm* const* comms, int world);
 int gp_comm_set_tuning(gp_comm* comm, int ctas_per_rank, double timeout_s);
 /* Optional ring timeline for profiling: device buffer of nlocal x ctas x 4 warps
  * x 20 u64 %globaltimer stamps (see csrc/ring.cuh kTraceSlots); NULL disables. */
 int gp_comm_set_trace(gp_comm* comm, void* device_buffer);
-int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, emulated] */);
+int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, mode (0 own GPU, 1 emulated, 2 per-rank launch on a shared GPU)] */);
 int gp_comm_destroy(gp_comm* comm);
 /* Test hook: set the device call counter of this communicator's inbox(es)
  * (sequence numbers cycle 1 .. 2^32-1; tests start near the wrap). Every rank

@@ -59,6 +59,15 @@ def _device_input(local, device: torch.device) -> torch.Tensor:
     return t
 
 
+def _rank_stream(endpoint: GpuEndpoint) -> torch.cuda.Stream:
+    """The endpoint's own stream, ordered after the caller's current stream
+    (which produced the inputs). Blocking calls run there so that ranks
+    sharing a GPU never serialise their launches on one stream."""
+    s = endpoint.stream
+    s.wait_stream(torch.cuda.current_stream(endpoint.device))
+    return s
+
+
 def allreduce_into(x: torch.Tensor, out: torch.Tensor | None, endpoint: GpuEndpoint, codec=Codec.NONE,
                    iteration: int = 0, stream: torch.cuda.Stream | None = None, precompress: bool = False,
                    slot: torch.Tensor | None = None, slot_scale: torch.Tensor | None = None) -> None:
@@ -92,7 +101,7 @@ def ring_allreduce(local, rank: int, p: int, endpoint: GpuEndpoint, codec: Codec
     with torch.cuda.device(dev):
         x = _device_input(local, dev)
         out = torch.empty_like(x)
-        s = torch.cuda.current_stream(dev)
+        s = _rank_stream(endpoint)
         allreduce_into(x, out, endpoint, codec, iteration, s)
         endpoint_wait(endpoint, x.numel(), s)
     return out.cpu().numpy() if as_numpy else out
@@ -117,7 +126,7 @@ def gather_to_root(local, root: int, rank: int, p: int, endpoint: GpuEndpoint, i
     with torch.cuda.device(dev):
         x = _device_input(local, dev)
         out = torch.empty_like(x) if rank == root else None
-        s = torch.cuda.current_stream(dev)
+        s = _rank_stream(endpoint)
         endpoint._star(x, out, x.numel(), root, 0, False, iteration, s)
         endpoint_wait(endpoint, x.numel(), s)
     if out is None:
@@ -135,11 +144,11 @@ def broadcast_from_root(value, root: int, rank: int, p: int, endpoint: GpuEndpoi
     as_numpy = rank == root and not isinstance(value, torch.Tensor)
     dev = endpoint.device
     with torch.cuda.device(dev):
-        s = torch.cuda.current_stream(dev)
         hdr = torch.zeros(4, dtype=torch.int32, device=dev)
         if rank == root:
             x = _device_input(value, dev)
             hdr[0] = x.numel()
+        s = _rank_stream(endpoint)
         got = torch.empty_like(hdr)
         endpoint._star(hdr.view(torch.float32), got.view(torch.float32), 4, root, 1, False, iteration, s)
         endpoint_wait(endpoint, 4, s)
@@ -148,6 +157,7 @@ def broadcast_from_root(value, root: int, rank: int, p: int, endpoint: GpuEndpoi
             x = torch.empty(n, dtype=torch.float32, device=dev)
             as_numpy = not isinstance(value, torch.Tensor) if value is not None else True
         out = torch.empty_like(x)
+        s = _rank_stream(endpoint)
         endpoint._star(x, out, n, root, 1, False, iteration, s)
         endpoint_wait(endpoint, n, s)
     return out.cpu().numpy() if as_numpy else out

@@ -71,6 +71,7 @@ struct gp_comm {
   uint64_t max_elems = 0;
   Layout L{};
   int nlocal = 1;                       // p when emulated
+  int share = 1;                        // per-rank communicators launched on this comm's device
   uint8_t* inbox[kMaxRanks] = {};       // local allocations (1, or p when emulated)
   uint8_t* peer[kMaxRanks] = {};        // every rank's inbox as mapped on this device
   bool ipc_opened[kMaxRanks] = {};
@@ -282,20 +283,30 @@ int gp_comm_connect_ipc(gp_comm* c, const void* handles) {
 
 int gp_comm_connect_local(gp_comm* const* comms, int world) {
   if (!comms || world < 1 || world > kMaxRanks) return fail(GP_ERR_ARG, "bad communicator list");
-  for (int i = 0; i < world; ++i) {
+  for (int i = 0; i < world; ++i)
     if (!comms[i] || comms[i]->world != world || comms[i]->rank != i || comms[i]->nlocal != 1)
       return fail(GP_ERR_ARG, "communicator list must hold ranks 0..world-1 of one world");
-    for (int k = 0; k < i; ++k)
-      if (comms[k]->device == comms[i]->device)
-        return fail(GP_ERR_UNSUPPORTED,
-                    "ranks " + std::to_string(k) + " and " + std::to_string(i) +
-                        " share device " + std::to_string(comms[i]->device) +
-                        "; use the emulated communicator for more ranks than GPUs");
+  // Ranks may share a GPU: each still gets its own inbox and its own ring
+  // launch (cudaLaunchKernel on its own stream, the per-rank path of a real
+  // multi-GPU run), and the device's SMs are split between them so that all
+  // their launches are resident at once (they wait on each other's flags).
+  for (int i = 0; i < world; ++i) {
+    int share = 0;
+    for (int k = 0; k < world; ++k) share += comms[k]->device == comms[i]->device;
+    comms[i]->share = share;
   }
+  int G = 1 << 30;
+  for (int i = 0; i < world; ++i) {
+    const int cap = std::max(1, sm_count(comms[i]->device) * ring_max_ctas_per_sm() / comms[i]->share);
+    G = std::min(G, std::min(comms[i]->G, cap));
+  }
+  for (int i = 0; i < world; ++i) comms[i]->G = G;  // chunking follows G: every rank agrees
   for (int i = 0; i < world; ++i) {
     DeviceGuard g(comms[i]->device);
     for (int k = 0; k < world; ++k) {
       if (k == i) continue;
+      comms[i]->peer[k] = comms[k]->inbox[0];
+      if (comms[k]->device == comms[i]->device) continue;  // same device: plain pointers
       int can = 0;
       cudaDeviceCanAccessPeer(&can, comms[i]->device, comms[k]->device);
       if (!can)
@@ -307,7 +318,6 @@ int gp_comm_connect_local(gp_comm* const* comms, int world) {
       } else if (e != cudaSuccess) {
         return cuda_fail(e, "cudaDeviceEnablePeerAccess");
       }
-      comms[i]->peer[k] = comms[k]->inbox[0];
     }
     comms[i]->connected = true;
   }
@@ -318,7 +328,7 @@ int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   if (ctas > 0) {
     // every CTA of one launch resident at once (emulated: all ranks' CTAs)
-    const int cap = std::max(1, sm_count(c->device) * ring_max_ctas_per_sm() / c->nlocal);
+    const int cap = std::max(1, sm_count(c->device) * ring_max_ctas_per_sm() / (c->nlocal * c->share));
     c->G = std::min(ctas, cap);
   }
   if (timeout_s > 0) c->timeout_s = timeout_s;
@@ -334,7 +344,7 @@ int gp_comm_set_trace(gp_comm* c, void* device_buffer) {
 int gp_comm_info(gp_comm* c, int64_t* o) {
   if (!c || !o) return fail(GP_ERR_ARG, "null argument");
   o[0] = c->rank; o[1] = c->world; o[2] = c->device; o[3] = (int64_t)c->max_elems;
-  o[4] = c->G; o[5] = (int64_t)c->L.total_bytes; o[6] = c->seq; o[7] = c->nlocal > 1;
+  o[4] = c->G; o[5] = (int64_t)c->L.total_bytes; o[6] = c->seq; o[7] = c->nlocal > 1 ? 1 : (c->share > 1 ? 2 : 0);
   return GP_OK;
 }
 

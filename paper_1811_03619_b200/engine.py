@@ -442,7 +442,11 @@ class RankEngine:
         self.static_loss = [torch.zeros((), dtype=torch.float32, device=self.dev) for _ in range(self.K)]
         self.g_update, self.g_compute, self.g_comm = [], [], []
         self.ev_agg = [torch.cuda.Event() for _ in range(self.K)]
-        torch.cuda.synchronize(self.dev)
+        # this rank's streams only: a device-wide sync could wait on a peer
+        # rank's ring that shares the GPU and waits for this rank's next call
+        torch.cuda.current_stream(self.dev).synchronize()
+        self.cs.synchronize()
+        self.ms.synchronize()
         if cfg.mode == MODE_D_SYNC:
             self._capture_sync_graphs(batches, lr)
             return

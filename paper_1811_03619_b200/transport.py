@@ -14,7 +14,10 @@ the 11-byte frame header).
 Three ways to build endpoints:
   * GpuTransport(world_size)            one process, rank r on cuda:r, peer
                                         access between all pairs (mirrors
-                                        InProcTransport: p threads, one per rank)
+                                        InProcTransport: p threads, one per rank);
+                                        devices=[0, 0, ...] puts several ranks on
+                                        one GPU, each still with its own inbox and
+                                        its own ring launch (SMs split between them)
   * EmulatedTransport(world_size)       p ranks on ONE GPU: the ranks' calls
                                         rendezvous and one cooperative launch
                                         runs the whole ring (parity at p > #GPUs)
@@ -76,6 +79,7 @@ class GpuEndpoint:
         self._transport = transport
         self._stats_base = TrafficStats()
         self._poisoned: str | None = None
+        self._stream: torch.cuda.Stream | None = None
         self.closed = False
 
     # -- reference Endpoint surface -------------------------------------
@@ -101,8 +105,17 @@ class GpuEndpoint:
         """Communicator facts: CTAs per rank, inbox bytes, calls issued."""
         o = (ctypes.c_int64 * 8)()
         _lib.call("gp_comm_info", self._comm, o)
-        keys = ("rank", "world", "device", "max_elems", "ctas", "inbox_bytes", "seq", "emulated")
+        keys = ("rank", "world", "device", "max_elems", "ctas", "inbox_bytes", "seq", "mode")
         return dict(zip(keys, [int(v) for v in o]))
+
+    @property
+    def stream(self) -> torch.cuda.Stream:
+        """The rank's own stream for the blocking entry points: ranks that share
+        a GPU must not queue their ring launches behind each other on one
+        stream (each waits for the others' flags)."""
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(self.device)
+        return self._stream
 
     # -- internals --------------------------------------------------------
     def _raw_stats(self) -> TrafficStats:
@@ -168,7 +181,13 @@ def raise_for(e, p: int, n: int, timeout_s: float) -> Exception:
 
 class GpuTransport:
     """In-process ring over p GPUs (rank r on devices[r]); threads play ranks,
-    exactly like the reference's InProcTransport (transport.py:150-177)."""
+    exactly like the reference's InProcTransport (transport.py:150-177).
+
+    Ranks may share a GPU (devices with repeats): every rank still launches
+    its own ring kernel on its own stream and reaches the others' inboxes
+    through plain device pointers, so the per-rank launch path (flag / LL
+    protocols, graph replay, sequence wrap) runs on a one-GPU box too; the
+    device's SMs are split so that all ranks' launches co-reside."""
 
     def __init__(self, world_size: int, latency_s: float = 0.0, byte_time_s: float = 0.0,
                  timeout_s: float = DEFAULT_TIMEOUT_S, devices=None, max_elems: int = DEFAULT_MAX_ELEMS,
@@ -180,9 +199,6 @@ class GpuTransport:
         devices = list(range(world_size)) if devices is None else list(devices)
         if len(devices) != world_size:
             raise ConfigError("need one device per rank")
-        if len(set(devices)) != world_size:
-            raise ConfigError("GpuTransport needs a distinct GPU per rank; use EmulatedTransport "
-                              "to run more ranks than GPUs")
         if torch.cuda.device_count() < max(devices) + 1:
             raise ConfigError(f"{world_size} ranks need {max(devices) + 1} GPUs, "
                               f"found {torch.cuda.device_count()}")

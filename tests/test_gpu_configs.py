@@ -92,13 +92,13 @@ def test_c4_resnet50_trunc16_p4_emulated(P):
     check_blocks(ins, outs, 1, [1])
 
 
-@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("codec,n", [(2, ALEXNET), (0, RESNET50)])
 def test_c3_c4_on_real_gpus(P, codec, n):
-    p = 4 if NGPU >= 4 else 2
+    """Per-rank launches (one GPU per rank, or ranks sharing GPUs)."""
+    p = 4
     base = make_inputs(p, n, 1e-3, 6)
-    ins = [x.to(f"cuda:{r}") for r, x in enumerate(base)]
-    tr = P.GpuTransport(p, timeout_s=120.0, max_elems=n)
+    tr = real_transport(P, p, timeout_s=120.0, max_elems=n)
+    ins = [x.to(tr.endpoint(r).device) for r, x in enumerate(base)]
     try:
         outs = run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, p, ep, P.Codec(codec), iteration=2))
     finally:
@@ -130,17 +130,16 @@ def test_c1_mnist_mlp_pipe_sgd_bit_exact(P):
         assert_bits_equal(r.params, want, f"rank {r.rank}")
 
 
-@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_c2_cnn_replicas_stay_identical(P):
     from paper_1811_03619_b200.engine import RankEngine, RunConfig
     from paper_1811_03619_b200.models import FlatModel, build_torch_model
     import threading
     p, T = 2, 6
-    tr = P.GpuTransport(p, timeout_s=60.0, max_elems=5_000_000)
+    tr = real_transport(P, p, timeout_s=60.0, max_elems=5_000_000)
     init_lock = threading.Lock()  # torch's RNG is process-global: seed + init one thread at a time
 
     def op(r, ep):
-        dev = torch.device("cuda", r)
+        dev = ep.device
         with torch.cuda.device(dev):
             with init_lock:
                 torch.manual_seed(0)
@@ -152,7 +151,8 @@ def test_c2_cnn_replicas_stay_identical(P):
             cfg = RunConfig(mode="pipe_sgd", iterations=T, learning_rate=0.01, codec="trunc16", batch_size=64)
             eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False)
             eng.run()
-            torch.cuda.synchronize(dev)
+            eng.cs.synchronize()
+            eng.ms.synchronize()
             ep._check_errors(fm.num_params)
             return fm.params.cpu().numpy()
 

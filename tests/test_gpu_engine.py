@@ -210,17 +210,17 @@ def test_star_collectives_match_reference_semantics(P):
         tr.close()
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_star_back_to_back_over_nvlink_across_sequence_wrap(P):
-    """Real per-GPU launches (no shared cooperative launch): back-to-back
+    """Real per-rank launches (no shared cooperative launch; one GPU per rank
+    or ranks sharing GPUs): back-to-back
     gathers with changing roots and back-to-back broadcasts stay exact,
     because a star call closes only once every reader acknowledged the
     staged bytes; started two calls before the 32-bit call sequence wraps."""
-    from helpers import run_ranks
+    from helpers import real_transport, run_ranks
     from paper_1811_03619_b200 import _lib
     from paper_1811_03619_b200.collective import broadcast_from_root, gather_to_root
-    p = min(torch.cuda.device_count(), 4)
-    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=1 << 20)
+    p = 4
+    tr = real_transport(P, p, timeout_s=30.0, max_elems=1 << 20)
     try:
         for r in range(p):
             _lib.call("gp_comm_set_call_counter", tr.endpoint(r)._comm, 0xFFFFFFFF - 2)

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import assert_bits_equal, run_ranks
+from helpers import assert_bits_equal, real_transport, run_ranks
 from oracle import codec as OC
 from oracle import ring as OR
 
@@ -49,7 +49,8 @@ def run_fused(P, tr, ins, codec, pre, slot, devices):
             out = torch.empty_like(x)
             sl = torch.full((n * w,), 0xAB, dtype=torch.uint8, device=dev) if slot else None
             sc = torch.full((1,), -1.0, device=dev) if slot else None
-            s = torch.cuda.current_stream(dev)
+            s = ep.stream  # the rank's own stream (ranks may share a GPU)
+            s.wait_stream(torch.cuda.current_stream(dev))
             allreduce_into(x, out, ep, codec, 4, s, precompress=pre, slot=sl, slot_scale=sc)
             endpoint_wait(ep, n, s)
             if slot:
@@ -92,13 +93,12 @@ def test_fused_variants_emulated(P, p):
         tr.close()
 
 
-@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("n", [4_710_538, 150_001])  # flag protocol / LL protocol
 @pytest.mark.parametrize("codec", [0, 1, 2])
 def test_fused_variants_p2p(P, codec, n):
-    p = 4 if NGPU >= 4 else 2
-    tr = P.GpuTransport(p, timeout_s=60.0, max_elems=n)
-    devs = [torch.device("cuda", r) for r in range(p)]
+    p = 4  # per-rank launches: one GPU per rank, or ranks sharing GPUs
+    tr = real_transport(P, p, timeout_s=60.0, max_elems=n)
+    devs = [tr.endpoint(r).device for r in range(p)]
     try:
         ins = inputs(p, n, 77 + codec, scale_exp=-3)
         for pre, slot in ((True, False), (True, True)):

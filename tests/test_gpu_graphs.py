@@ -1,13 +1,14 @@
 """CUDA-graph replay of the pipelined step (RankEngine.capture_graphs /
 step_graph) computes exactly what the eager engine computes: same weights,
-bit for bit, after warm-up + graph steps + drain, for p = 1 and (with two
-GPUs) p = 2 over NVLink, every codec."""
+bit for bit, after warm-up + graph steps + drain, for p = 1 and p = 2
+(per-rank launches: over NVLink with two GPUs, else both ranks on one GPU),
+every codec."""
 
 import numpy as np
 import pytest
 import torch
 
-from helpers import assert_bits_equal, run_ranks
+from helpers import assert_bits_equal, real_transport, run_ranks
 
 pytestmark = pytest.mark.gpu
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
@@ -17,10 +18,10 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0):
     from paper_1811_03619_b200.engine import RankEngine, RunConfig
     from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
     spec = ModelSpec("mlp", (64, 128, 10))
-    tr = P.GpuTransport(p, timeout_s=30.0, max_elems=spec.num_params, ctas=64)
+    tr = real_transport(P, p, timeout_s=30.0, max_elems=spec.num_params, ctas=64)
 
     def op(r, ep):
-        dev = torch.device("cuda", r)
+        dev = ep.device
         with torch.cuda.device(dev):
             fm = FlatModel(SpecNet(spec), dev, init_params(spec, 1))
             g = torch.Generator(device="cpu").manual_seed(10 + r)
@@ -45,7 +46,8 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0):
                     for t in range(W + 1, T + 1):
                         step(t)
                     eng.drain(T) if pipe else eng.drain_sync()
-            torch.cuda.synchronize(dev)
+            eng.cs.synchronize()
+            eng.ms.synchronize()
             ep._check_errors(fm.num_params)
             return fm.params.cpu().numpy(), eng.losses[1:T + 1].cpu().numpy()
 
@@ -59,8 +61,6 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0):
 @pytest.mark.parametrize("codec", [0, 1, 2])
 @pytest.mark.parametrize("p", [1, 2])
 def test_graph_replay_matches_eager(P, p, codec, mode):
-    if p > NGPU:
-        pytest.skip("needs more GPUs")
     eager = train(P, p, codec, graphs=False, mode=mode)
     graph = train(P, p, codec, graphs=True, mode=mode)
     for r in range(p):
@@ -73,8 +73,6 @@ def test_graph_replay_matches_eager(P, p, codec, mode):
 @pytest.mark.parametrize("codec", [1, 2])
 @pytest.mark.parametrize("p", [1, 2])
 def test_graph_replay_width_3_matches_eager(P, p, codec):
-    if p > NGPU:
-        pytest.skip("needs more GPUs")
     eager = train(P, p, codec, graphs=False, depth=3)
     graph = train(P, p, codec, graphs=True, depth=3)
     for r in range(p):
@@ -88,8 +86,6 @@ def test_graph_replay_with_lr_decay_matches_eager(P, p, mode):
     """engine.py:287-292 decay under replay: the update graphs read the rate
     from device memory, written before every replay; the drain uses the
     eager engine's per-tag rates."""
-    if p > NGPU:
-        pytest.skip("needs more GPUs")
     eager = train(P, p, 1, graphs=False, mode=mode, decay=4)
     graph = train(P, p, 1, graphs=True, mode=mode, decay=4)
     for r in range(p):
