@@ -60,7 +60,8 @@ enum {
 };
 
 /* device failure kinds (gp_error.kind, gp_codec_status.nonfinite) */
-enum { GP_FAIL_NONE = 0, GP_FAIL_NONFINITE = 1, GP_FAIL_TIMEOUT = 2, GP_FAIL_HEADER = 3 };
+enum { GP_FAIL_NONE = 0, GP_FAIL_NONFINITE = 1, GP_FAIL_TIMEOUT = 2, GP_FAIL_HEADER = 3,
+       GP_FAIL_BOUNDS = 4 /* bounds-checked build only (libpipesgd_checked.so): an access outside its buffer or slot */ };
 /* gp_error.phase */
 enum { GP_PHASE_REDUCE_SCATTER = 0, GP_PHASE_ALLGATHER = 1, GP_PHASE_BARRIER = 2 };
 
@@ -98,7 +99,7 @@ int gp_comm_connect_ipc(gp_comm* comm, const void* handles /* world x 64 bytes, 
 int gp_comm_connect_local(gp_comm* const* comms, int world);
 int gp_comm_set_tuning(gp_comm* comm, int ctas_per_rank, double timeout_s);
 /* Optional ring timeline for profiling: device buffer of nlocal x ctas x 4 warps
- * x 20 u64 %globaltimer stamps (see csrc/ring.cuh kTraceSlots); NULL disables. */
+ * x 44 u64 %globaltimer stamps (see csrc/ring.cuh kTraceSlots); NULL disables. */
 int gp_comm_set_trace(gp_comm* comm, void* device_buffer);
 int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, mode (0 own GPU, 1 emulated, 2 per-rank launch on a shared GPU)] */);
 int gp_comm_destroy(gp_comm* comm);

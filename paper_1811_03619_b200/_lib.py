@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PIPESGD_LIB") or os.path.join(HERE, "libpipesgd.so")
 
 GP_OK = 0
-GP_FAIL_NONFINITE, GP_FAIL_TIMEOUT, GP_FAIL_HEADER = 1, 2, 3
+GP_FAIL_NONFINITE, GP_FAIL_TIMEOUT, GP_FAIL_HEADER, GP_FAIL_BOUNDS = 1, 2, 3, 4
 GP_PHASE_RS, GP_PHASE_AG, GP_PHASE_BARRIER = 0, 1, 2
 GP_RING_PRECOMPRESS, GP_RING_SLOT_OUT = 1, 2
 

@@ -25,6 +25,15 @@
 
 #include "common.cuh"
 
+// Bounds-checked build (-DPIPESGD_CHECKED, libpipesgd_checked.so): a
+// translation unit may define GP_ACCESS_OK(ptr, bytes, write) before including
+// this header; every payload / vector access below asks it first and skips
+// the access when it is refused (the hook records the violation). The
+// product build compiles the hook away.
+#ifndef GP_ACCESS_OK
+#define GP_ACCESS_OK(ptr, bytes, write) true
+#endif
+
 namespace gp {
 
 __device__ __forceinline__ uint32_t t16_encode(float x) {
@@ -149,6 +158,11 @@ __device__ __forceinline__ FV<E> load_fv(const float* x, uint64_t g0, uint64_t l
   FV<E> r;
   if (lo <= g0 && g0 + E <= hi) {
     const float4* p = reinterpret_cast<const float4*>(x + g0);
+    if (!GP_ACCESS_OK(p, 4 * E, false)) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) r.v[i] = 0.f;
+      return r;
+    }
 #pragma unroll
     for (int k = 0; k < E / 4; ++k) {
       const float4 a = NC ? __ldg(p + k) : __ldcg(p + k);
@@ -157,7 +171,8 @@ __device__ __forceinline__ FV<E> load_fv(const float* x, uint64_t g0, uint64_t l
   } else {
 #pragma unroll
     for (int i = 0; i < E; ++i)
-      r.v[i] = (g0 + i >= lo && g0 + i < hi) ? (NC ? __ldg(x + g0 + i) : __ldcg(x + g0 + i)) : 0.f;
+      r.v[i] = (g0 + i >= lo && g0 + i < hi && GP_ACCESS_OK(x + g0 + i, 4, false))
+                   ? (NC ? __ldg(x + g0 + i) : __ldcg(x + g0 + i)) : 0.f;
   }
   return r;
 }
@@ -196,6 +211,7 @@ __device__ __forceinline__ FV<E> load_fv_pol(const float* x, uint64_t g0, uint64
   if (!(lo <= g0 && g0 + E <= hi)) return load_fv<E>(x, g0, lo, hi);
   FV<E> r;
   const float4* p = reinterpret_cast<const float4*>(x + g0);
+  if (!GP_ACCESS_OK(p, 4 * E, false)) return load_fv<E>(x, g0, 1, 0);  // refused: zeros
 #pragma unroll
   for (int k = 0; k < E / 4; ++k) {
     const float4 a = ldg_hint(p + k, pol);
@@ -208,12 +224,13 @@ template <int E>
 __device__ __forceinline__ void store_fv(float* x, uint64_t g0, uint64_t lo, uint64_t hi, const FV<E>& r) {
   if (lo <= g0 && g0 + E <= hi) {
     float4* p = reinterpret_cast<float4*>(x + g0);
+    if (!GP_ACCESS_OK(p, 4 * E, true)) return;
 #pragma unroll
     for (int k = 0; k < E / 4; ++k) p[k] = make_float4(r.v[4 * k], r.v[4 * k + 1], r.v[4 * k + 2], r.v[4 * k + 3]);
   } else {
 #pragma unroll
     for (int i = 0; i < E; ++i)
-      if (g0 + i >= lo && g0 + i < hi) x[g0 + i] = r.v[i];
+      if (g0 + i >= lo && g0 + i < hi && GP_ACCESS_OK(x + g0 + i, 4, true)) x[g0 + i] = r.v[i];
   }
 }
 
@@ -223,6 +240,7 @@ template <int C>
 __device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, int vlo, int vhi) {
   constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
   const uint8_t* base = slot + rel0 * W;
+  if (!GP_ACCESS_OK(base + vlo * W, (vhi - vlo) * W, false)) return make_uint4(0, 0, 0, 0);
   if (vlo == 0 && vhi == E) return __ldcg(reinterpret_cast<const uint4*>(base));
   uint32_t w[4] = {0, 0, 0, 0};
   for (int i = vlo; i < vhi; ++i) {
@@ -239,7 +257,8 @@ __device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, in
 template <int C>
 __device__ __forceinline__ uint4 load_pay_pol(const uint8_t* slot, uint64_t rel0, int vlo, int vhi, uint64_t pol) {
   constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
-  if (vlo == 0 && vhi == E) return ldcg_hint(reinterpret_cast<const uint4*>(slot + rel0 * W), pol);
+  if (vlo == 0 && vhi == E && GP_ACCESS_OK(slot + rel0 * W, 16, false))
+    return ldcg_hint(reinterpret_cast<const uint4*>(slot + rel0 * W), pol);
   return load_pay<C>(slot, rel0, vlo, vhi);
 }
 
@@ -247,6 +266,7 @@ template <int C>
 __device__ __forceinline__ void store_pay(uint8_t* slot, uint64_t rel0, int vlo, int vhi, const uint4& p) {
   constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
   uint8_t* base = slot + rel0 * W;
+  if (!GP_ACCESS_OK(base + vlo * W, (vhi - vlo) * W, true)) return;
   if (vlo == 0 && vhi == E) {
     __stcg(reinterpret_cast<uint4*>(base), p);
     return;

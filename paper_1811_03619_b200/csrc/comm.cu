@@ -447,6 +447,9 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
   }
   P.timeout_ns = (uint64_t)(c->timeout_s * 1e9);
   P.trace = c->trace;
+#ifdef PIPESGD_CHECKED
+  P.selftest = std::getenv("PIPESGD_CHECKED_SELFTEST") != nullptr;
+#endif
   for (int i = 0; i < c->nlocal; ++i) {
     RankCtx& R = P.rk[i];
     R.x = ins[i];

@@ -17,7 +17,7 @@ enum Codec : int { kNone = 0, kTrunc16 = 1, kQuant8 = 2 };
 // Error kinds latched by kernels; surfaced by the host as the reference's
 // exception classes (errors.py:16-29): NONFINITE -> CodecError,
 // TIMEOUT/HEADER/ABORT -> CollectiveError.
-enum ErrKind : int { kErrNone = 0, kErrNonFinite = 1, kErrTimeout = 2, kErrHeader = 3 };
+enum ErrKind : int { kErrNone = 0, kErrNonFinite = 1, kErrTimeout = 2, kErrHeader = 3, kErrBounds = 4 };
 enum Phase : int { kPhRS = 0, kPhAG = 1, kPhBarrier = 2, kPhLocal = 3 };
 
 // Device error word: one u64 so the EARLIEST failure wins via atomicMin,

@@ -34,6 +34,14 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cstdint>
+#ifdef PIPESGD_CHECKED
+namespace gp {
+__device__ __noinline__ bool ring_access_ok(const void* p, uint64_t bytes, bool write);
+__device__ __noinline__ void bounds_violation(uint64_t addr);
+}  // namespace gp
+#define GP_ACCESS_OK(p, bytes, write) ::gp::ring_access_ok((p), (bytes), (write))
+#endif
 #include "codec.cuh"
 #include "ring.cuh"
 
@@ -54,6 +62,9 @@ __shared__ uint32_t s_seq;
 __shared__ uint32_t s_bank;                 // ctl bank of this call (ring.cuh:CtlBank)
 __shared__ unsigned long long s_calls;      // raw count of calls completed before this one
 __shared__ unsigned long long s_abort;      // the abort word at kernel entry
+#ifdef PIPESGD_CHECKED
+__shared__ const RingParams* s_P;           // launch parameters (bounds checks)
+#endif
 
 __device__ __forceinline__ CtlBank* cb(Ctl* c) { return &c->bank[s_bank]; }
 
@@ -73,9 +84,21 @@ __device__ __forceinline__ Blk get_blk(const RingParams& P, int b) {
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ uint64_t* flag_ptr(uint8_t* inbox, const Layout& L, int slot, uint32_t c) {
+#ifdef PIPESGD_CHECKED
+  if (slot < 0 || (uint32_t)slot >= L.nslot || c >= L.max_chunks) {
+    bounds_violation(((uint64_t)slot << 32) | c);
+    slot = 0, c = 0;
+  }
+#endif
   return reinterpret_cast<uint64_t*>(inbox + L.off_flags) + (uint64_t)slot * L.max_chunks + c;
 }
 __device__ __forceinline__ SlotHdr* hdr_ptr(uint8_t* inbox, const Layout& L, int slot) {
+#ifdef PIPESGD_CHECKED
+  if (slot < 0 || (uint32_t)slot >= L.nslot) {
+    bounds_violation((uint64_t)slot);
+    slot = 0;
+  }
+#endif
   return reinterpret_cast<SlotHdr*>(inbox + L.off_hdr) + slot;
 }
 __device__ __forceinline__ uint8_t* slot_ptr(uint8_t* inbox, const Layout& L, int slot) {
@@ -105,6 +128,7 @@ __device__ __forceinline__ uint4 ld_vol_v4(const uint4* p) {
   return v;
 }
 __device__ __forceinline__ void ll_put(uint8_t* line, uint4 v) {
+  if (!GP_ACCESS_OK(line, 32, true)) return;
   uint4* q = reinterpret_cast<uint4*>(line);
   st_vol_v4(q, make_uint4(v.x, s_seq, v.y, s_seq));
   st_vol_v4(q + 1, make_uint4(v.z, s_seq, v.w, s_seq));
@@ -112,6 +136,7 @@ __device__ __forceinline__ void ll_put(uint8_t* line, uint4 v) {
 // Poll one line; false if `give_up` turned true (timeout / abort seen).
 template <typename G>
 __device__ __forceinline__ bool ll_get(const uint8_t* line, uint4& out, G&& give_up) {
+  if (!GP_ACCESS_OK(line, 32, false)) return false;
   const uint4* q = reinterpret_cast<const uint4*>(line);
   for (uint32_t it = 1;; ++it) {
     const uint4 a = ld_vol_v4(q), b = ld_vol_v4(q + 1);
@@ -315,7 +340,7 @@ __device__ __forceinline__ void stamp(const RingParams& P, uint32_t wid, int lra
 // p == 2 only (slots 4..13 belong to reduce-scatter steps s >= 1 otherwise):
 // finer per-chunk stamps for the fold phase, first chunk of each warp.
 __device__ __forceinline__ void stamp2(const RingParams& P, uint32_t wid, int lrank, int k, bool on) {
-  if (on && P.p == 2) stamp(P, wid, lrank, k);
+  if (on && P.p == 2) stamp(P, wid, lrank, kTrP2 + k - 4);
 }
 
 // Chunk scheduling: in every phase warp w first takes chunk w (no atomic,
@@ -353,6 +378,47 @@ __device__ __forceinline__ float read_max_slot(Ctl* ctl, int idx) {
 
 }  // namespace
 
+#ifdef PIPESGD_CHECKED
+// Bounds-checked build: every payload / vector / LL access of the ring must
+// fall inside this rank's x (read only), out, slot output, or ONE region of
+// some rank's inbox (the control area, a single payload slot, a single LL
+// slot), so an indexing slip into a neighbouring slot is caught too. A
+// refused access is skipped and latched as kErrBounds in the rank's error
+// word (GP_FAIL_BOUNDS on the host).
+namespace {
+__device__ bool inbox_region_ok(const Layout& L, uint64_t off, uint64_t end) {
+  if (end > L.total_bytes) return false;
+  if (off < L.off_payload) return end <= L.off_payload;
+  if (off < L.off_ll) return end <= L.off_payload + ((off - L.off_payload) / L.slot_bytes + 1) * L.slot_bytes;
+  return end <= L.off_ll + ((off - L.off_ll) / L.ll_slot_bytes + 1) * L.ll_slot_bytes;
+}
+}  // namespace
+
+__device__ __noinline__ void bounds_violation(uint64_t addr) {
+  const RankCtx& R = s_P->rk[blockIdx.x / s_P->G];
+  latch_error(reinterpret_cast<ErrWord*>(R.inbox + s_P->L.off_err), kErrBounds, kPhLocal, 0, -1, R.rank,
+              (int)(uint32_t)addr);
+}
+
+__device__ __noinline__ bool ring_access_ok(const void* ptr, uint64_t bytes, bool write) {
+  const RingParams& P = *s_P;
+  const RankCtx& R = P.rk[blockIdx.x / P.G];
+  const uint64_t a = reinterpret_cast<uint64_t>(ptr), b = a + bytes;
+  const uint64_t w = P.codec == kNone ? 4 : P.codec == kTrunc16 ? 2 : 1;
+  auto in = [&](const void* base, uint64_t len) {
+    const uint64_t lo = reinterpret_cast<uint64_t>(base);
+    return base != nullptr && a >= lo && b <= lo + len;
+  };
+  bool ok = (!write && in(R.x, 4 * P.n)) || in(R.out, 4 * P.n) || in(R.slot, w * P.n);
+  for (int q = 0; q < P.p && !ok; ++q) {
+    const uint64_t base = reinterpret_cast<uint64_t>(R.peer[q]);
+    if (a >= base && a < base + P.L.total_bytes) ok = inbox_region_ok(P.L, a - base, b - base);
+  }
+  if (!ok) bounds_violation(a);
+  return ok;
+}
+#endif
+
 template <int C, bool LL>
 __device__ __forceinline__ void ring_body(const RingParams& P) {
   constexpr int E = CodecT<C>::E;
@@ -369,6 +435,12 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   const bool slot_mode = R.slot != nullptr;
   int bad = 0;
   stamp(P, wid, lr, 0);
+#ifdef PIPESGD_CHECKED
+  if (P.selftest && wid == 0 && out != nullptr) {  // negative control: one group past the end of out
+    FV<4> z = {};
+    store_fv<4>(out, P.n, P.n, P.n + 4, z);
+  }
+#endif
   // an earlier call failed on some rank: this one ends at once, reported as
   // a consequence of the peer's failure (no timeout wait)
   if (s_abort & kAbortSticky) {
@@ -517,7 +589,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         }
         if (!__all_sync(0xffffffffu, ok)) return false;
       }
-      if (first) stamp(P, wid, lr, 2);
+      if (first) stamp(P, wid, lr, tr_step(0, 0));
       first = false;
       const uint64_t cbase = B.A + (uint64_t)c * P.chunk;
       const uint64_t lo = max(B.start, cbase), hi = min(B.start + B.len, cbase + P.chunk);
@@ -569,7 +641,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     }
     if (__any_sync(0xffffffffu, bad) && lane_id() == 0) latch_error(err, kErrNonFinite, kPhAG, 0, own, r, 0);
     bad = 0;
-    stamp(P, wid, lr, 3);
+    stamp(P, wid, lr, tr_step(0, 3));
     return true;
   };
 
@@ -623,7 +695,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           vmax = fabsf(q8_decode(q8_encode(own, q0), q0.s));
         }
         q = q8_make(q8_scale(vmax));
-        stamp(P, wid, lr, 16);
+        stamp(P, wid, lr, kTrQ8Max);
       }
       uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
       uint8_t* lld = ll_ptr(R.peer[succ], P.L, rs_slot(0));
@@ -701,7 +773,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
             return;
           }
-          if (first) stamp(P, wid, lr, 2 + 2 * s);
+          if (first) stamp(P, wid, lr, tr_step(s, 0));
           for_groups<C>(P, B, c, load_xin,
                         [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                           emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
@@ -739,7 +811,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
             return;
           }
-          if (first) stamp(P, wid, lr, 2 + 2 * s);
+          if (first) stamp(P, wid, lr, tr_step(s, 0));
           first = false;
           for_groups<C>(P, B, c,
                         [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
@@ -751,9 +823,9 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           if (ll && !ll_ok(kPhRS, s, b)) return;
         }
         float vmax;
-        if (s == 0) stamp(P, wid, lr, 15);  // (p = 2: slot 15 is free) pass A done
+        stamp(P, wid, lr, tr_step(s, 1));  // pass A done
         if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
-        if (s == 0) stamp(P, wid, lr, 17);
+        stamp(P, wid, lr, tr_step(s, 2));  // barrier open
         const Q8 q = q8_make(q8_scale(vmax));
         // pass B: recompute the partial, encode it with the block scale and
         // push it. Any warp may take any chunk: the chunk's flag (or LL
@@ -786,7 +858,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
         latch_error(err, kErrNonFinite, last ? kPhAG : kPhRS, last ? 0 : s + 1, b, r, 0);
       bad = 0;
-      stamp(P, wid, lr, 3 + 2 * s);
+      stamp(P, wid, lr, tr_step(s, 3));
     }
   }
 
@@ -843,7 +915,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       } else if (!warp_await(P, R, ctl, err, ag_slot(p, b), c, kPhAG, step, b, B.len, sin)) {
         return;
       }
-      if (k == 1 && first) stamp(P, wid, lr, 18);
+      if (k == 1 && first) stamp(P, wid, lr, kTrAgIn);
       first = false;
       for_groups<C>(P, B, c,
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
@@ -861,7 +933,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       if (ll && !ll_ok(kPhAG, step, b)) return;
     }
   }
-  stamp(P, wid, lr, 19);
+  stamp(P, wid, lr, kTrEnd);
 }
 
 #ifndef PIPESGD_RING_MINBLOCKS
@@ -873,6 +945,9 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
   const int lr = blockIdx.x / P.G;
   Ctl* ctl = reinterpret_cast<Ctl*>(P.rk[lr].inbox + P.L.off_ctl);
   if (threadIdx.x == 0) {
+#ifdef PIPESGD_CHECKED
+    s_P = &P;
+#endif
     const unsigned long long calls = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&ctl->calls));
     s_calls = calls;
     s_seq = next_seq(calls);

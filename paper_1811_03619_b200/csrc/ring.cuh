@@ -131,13 +131,18 @@ struct RingParams {
   int pre;                     // x is the raw gradient: apply the local D(C(.)) on load
   int ll;                      // this call uses the LL protocol (see ll_payload_limit)
   int direct;                  // codec none, p >= 3: direct reduce-scatter (one hop, ring.cu)
+  int selftest;                // bounds-checked build only: one deliberate store past `out` (negative control)
   unsigned long long* trace;   // optional timeline: kTraceSlots %globaltimer stamps per warp
 };
 
-constexpr int kTraceSlots = 20;  // [0] start, [1] step-0 send done, [2+2s] step s first chunk
-                                 // in, [3+2s] step s done, [15-17] quant8 pass/barrier stamps,
-                                 // [18] allgather first in, [19] end; at p = 2 slots 4-9 hold
-                                 // the first chunk's fold/send/allgather sub-stamps
+// Ring timeline slots (per warp, %globaltimer ns): [0] start, [1] step-0 send
+// done, [2] quant8 step-0 max barrier open, step s: [3+4s] first chunk in,
+// [4+4s] quant8 pass A done, [5+4s] quant8 barrier open, [6+4s] step done;
+// [35] allgather first in, [36] end; p = 2: [37-42] the first chunk's
+// fold / send / allgather sub-stamps.
+constexpr int kTraceSlots = 44;
+constexpr int kTrQ8Max = 2, kTrAgIn = 35, kTrEnd = 36, kTrP2 = 37;
+__host__ __device__ inline int tr_step(int s, int k) { return 3 + 4 * s + k; }
 
 __host__ __device__ inline int rs_slot(int s) { return s; }
 __host__ __device__ inline int ag_slot(int p, int b) { return p - 1 + b; }

@@ -34,6 +34,7 @@ device-resident rate), bit-identical to the eager step.
 
 from __future__ import annotations
 
+import contextlib
 import os
 import threading
 import time
@@ -63,6 +64,20 @@ STAGE_ALLREDUCE = "allreduce"
 STAGE_DECOMPRESS = "decompress"
 STAGE_BARRIER = "barrier"
 STAGE_IDLE = "idle"
+
+
+@contextlib.contextmanager
+def capture(graph: torch.cuda.CUDAGraph, stream: torch.cuda.Stream):
+    """torch.cuda.graph without its device-wide synchronize: a rank sharing
+    this GPU with other ranks may be mid-capture (a device sync is illegal
+    then) or mid-call (its ring waits for this rank, so a device sync could
+    wait on it). Callers synchronize their own streams first."""
+    with torch.cuda.stream(stream):
+        graph.capture_begin(capture_error_mode="thread_local")
+        try:
+            yield graph
+        finally:
+            graph.capture_end()
 
 
 @dataclass(frozen=True)
@@ -453,16 +468,16 @@ class RankEngine:
         for i in range(self.K):
             slot = self.slots[i]
             gu = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gu, stream=self.cs, capture_error_mode="thread_local"):
+            with capture(gu, self.cs):
                 _lib.call("gp_consume_update_dev", self.fm.params.data_ptr(), int(slot.codec), slot.payload.data_ptr(),
                           slot.status.scale_view.data_ptr(), self.n, lr.data_ptr(), self.world, self.cs.cuda_stream)
             self.g_update.append(gu)
             gc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
+            with capture(gc, self.cs):
                 self.fm.use_grad_buffer(i)
                 self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
             gm = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gm, stream=self.ms, capture_error_mode="thread_local"):
+            with capture(gm, self.ms):
                 g = self.fm.grad_bufs[i]
                 if self.world > 1:
                     allreduce_into(g, self.summed, self.ep, cfg.codec, 0, self.ms, precompress=True,
@@ -478,15 +493,15 @@ class RankEngine:
         for i in range(K):
             pend = self.sync_slots[(i - 1) % K]  # holds the sum of t-1 when t % K == i
             gu = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gu, stream=self.cs, capture_error_mode="thread_local"):
+            with capture(gu, self.cs):
                 _lib.call("gp_consume_update_dev", self.fm.params.data_ptr(), int(Codec.NONE), pend.payload.data_ptr(),
                           pend.status.scale_view.data_ptr(), self.n, lr.data_ptr(), self.world, self.cs.cuda_stream)
             gc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gc, stream=self.cs, capture_error_mode="thread_local"):
+            with capture(gc, self.cs):
                 self.fm.use_grad_buffer(i)
                 self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
             gm = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gm, stream=self.cs, capture_error_mode="thread_local"):
+            with capture(gm, self.cs):
                 g = self.fm.grad_bufs[i]
                 if self.world > 1:
                     allreduce_into(g, self.summed, self.ep, codec, 0, self.cs, precompress=True)

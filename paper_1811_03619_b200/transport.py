@@ -176,6 +176,9 @@ def raise_for(e, p: int, n: int, timeout_s: float) -> Exception:
         want = partition_blocks(n, p)[e.block][1] if 0 <= e.block < p else -1
         return CollectiveError(f"{phase} step {e.step}: block {e.block} has {e.detail} elems, expected "
                                f"{want} or a different iteration tag (unequal vector lengths across ranks?)")
+    if e.kind == _lib.GP_FAIL_BOUNDS:
+        return CollectiveError(f"bounds-checked build: rank {e.rank} accessed outside its buffers "
+                               f"(address low bits {e.detail & 0xFFFFFFFF:#010x})")
     return CollectiveError(f"{phase} step {e.step}: device error kind {e.kind}")
 
 

@@ -5,11 +5,11 @@ C1  MNIST MLP 784-500-500-10 (648,010 params), p=4, codec none, Pipe-SGD
     oracle supplies the gradients.
 C3  AlexNet-sized gradient (61,100,840 fp32), quant8 ring at p=8 (emulated
     on one GPU) and on the real GPUs: every rank bit-identical, and sampled
-    ring blocks bit-exact with the oracle's fold (block b folds from rank b;
+    every ring block bit-exact with the oracle's fold (block b folds from rank b;
     the block-wide quant8 scale makes each block self-contained, so checking
     whole blocks is exact at full size).
 C4  ResNet-50-sized gradient (25,557,032), codec none, p=4 and 8: ranks
-    identical, sampled blocks bit-exact, and the sum within the reference's
+    identical, every block bit-exact, and the sum within the reference's
     own tolerance of the float64 direct sum (test_collective.py:50-54).
 C2  the bench's CIFAR CNN through the width-2 engine on real GPUs: replicas
     stay bit-identical over steps.
@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import assert_bits_equal, run_ranks
+from helpers import assert_bits_equal, real_transport, run_ranks
 from oracle import codec as OC
 from oracle import engine as OE
 from oracle import ring as OR
@@ -50,16 +50,24 @@ def oracle_block(ins_cpu_block, b, codec):
     return OC.roundtrip(s, codec)
 
 
-def check_blocks(ins, outs, codec, blocks_to_check):
+def check_blocks(ins, outs, codec):
+    """Every rank identical, and EVERY block bit-exact with the oracle's
+    fold (blocks are independent: the oracle folds them on threads)."""
+    from concurrent.futures import ThreadPoolExecutor
     p, n = len(ins), ins[0].numel()
     parts = OR.partition_blocks(n, p)
     for r in range(1, p):
         assert torch.equal(outs[r].view(torch.int32).to(outs[0].device), outs[0].view(torch.int32)), r
-    for b in blocks_to_check:
+    host = [x.cpu().numpy() for x in ins]
+    got = outs[0].cpu().numpy()
+
+    def one(b):
         off, ln = parts[b]
-        blk = [x[off:off + ln].cpu().numpy() for x in ins]
-        want = oracle_block(blk, b, codec)
-        assert_bits_equal(outs[0][off:off + ln].cpu().numpy(), want, f"block {b}")
+        want = oracle_block([h[off:off + ln] for h in host], b, codec)
+        assert_bits_equal(got[off:off + ln], want, f"block {b}")
+
+    with ThreadPoolExecutor(min(p, 8)) as pool:
+        list(pool.map(one, range(p)))
 
 
 def run_emulated(P, ins, codec, p):
@@ -73,13 +81,13 @@ def run_emulated(P, ins, codec, p):
 def test_c3_alexnet_quant8_p8_emulated(P):
     ins = make_inputs(8, ALEXNET, 1e-3, 3)
     outs = run_emulated(P, ins, P.Codec.QUANT8, 8)
-    check_blocks(ins, outs, 2, [0, 5])
+    check_blocks(ins, outs, 2)
 
 
 def test_c4_resnet50_none_p8_emulated(P):
     ins = make_inputs(8, RESNET50, 1e-2, 4)
     outs = run_emulated(P, ins, P.Codec.NONE, 8)
-    check_blocks(ins, outs, 0, [3])
+    check_blocks(ins, outs, 0)
     want = torch.stack(ins).double().sum(0)
     got = outs[0].double()
     atol = 1e-6 * max(1.0, want.abs().max().item())
@@ -89,7 +97,7 @@ def test_c4_resnet50_none_p8_emulated(P):
 def test_c4_resnet50_trunc16_p4_emulated(P):
     ins = make_inputs(4, RESNET50, 1e-2, 5)
     outs = run_emulated(P, ins, P.Codec.TRUNC16, 4)
-    check_blocks(ins, outs, 1, [1])
+    check_blocks(ins, outs, 1)
 
 
 @pytest.mark.parametrize("codec,n", [(2, ALEXNET), (0, RESNET50)])
@@ -103,7 +111,7 @@ def test_c3_c4_on_real_gpus(P, codec, n):
         outs = run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, p, ep, P.Codec(codec), iteration=2))
     finally:
         tr.close()
-    check_blocks(base, outs, codec, [0, p - 1])
+    check_blocks(base, outs, codec)
 
 
 def test_c1_mnist_mlp_pipe_sgd_bit_exact(P):
@@ -130,6 +138,8 @@ def test_c1_mnist_mlp_pipe_sgd_bit_exact(P):
         assert_bits_equal(r.params, want, f"rank {r.rank}")
 
 
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs: on one GPU a rank's spinning ring CTAs can starve the peer "
+                                     "rank's large cuDNN kernels that the ring is waiting for")
 def test_c2_cnn_replicas_stay_identical(P):
     from paper_1811_03619_b200.engine import RankEngine, RunConfig
     from paper_1811_03619_b200.models import FlatModel, build_torch_model
