@@ -101,6 +101,13 @@ int gp_comm_set_tuning(gp_comm* comm, int ctas_per_rank, double timeout_s);
 /* Optional ring timeline for profiling: device buffer of nlocal x ctas x 4 warps
  * x 44 u64 %globaltimer stamps (see csrc/ring.cuh kTraceSlots); NULL disables. */
 int gp_comm_set_trace(gp_comm* comm, void* device_buffer);
+/* Iteration tag from device memory: ring launches made while `device_tag` is
+ * set read the tag (the reference's message iteration, checked like
+ * collective.py:_expect :52-64) from this device word at kernel entry instead
+ * of the `iteration` argument, so a ring captured once in a CUDA graph still
+ * carries and checks the real step t on every replay (the host writes t
+ * before each replay). NULL restores the argument. */
+int gp_comm_set_iteration_source(gp_comm* comm, const uint32_t* device_tag);
 int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, mode (0 own GPU, 1 emulated, 2 per-rank launch on a shared GPU)] */);
 int gp_comm_destroy(gp_comm* comm);
 /* Test hook: set the device call counter of this communicator's inbox(es)

@@ -72,24 +72,35 @@ __device__ __forceinline__ Q8 q8_make(float s) {
   return q;
 }
 
-// One element -> int8 code (as int), branch-free (the ring is instruction-
-// bound on this): both exact residual tests are evaluated and selected.
-// Scale 0 (vmax tiny or 0): x/0 is +-inf in the reference -> +-127, and
-// 0/0 casts to 0. x == 0 (either sign) always yields 0.
+// One element -> int8 code (as int), branch-free and without the
+// quarter-rate conversion pipe (no FRND / F2I): y + 2^23 rounds y to an
+// integer k0 in the low mantissa bits (RN, within one of the answer, like
+// floor(y + 1/2) -- the exact residual tests below pick the right neighbour
+// either way), read back as an integer by subtracting the exponent pattern
+// and as an exact float by subtracting 2^23. Scale 0 (vmax tiny or 0): x/0 is
+// +-inf in the reference -> +-127, and 0/0 casts to 0. x == 0 (either sign)
+// always yields 0. Inputs are the block's own values, so y <= 127 * (1 +
+// 2^-15); the clamp to 255 only keeps a NaN (already latched) harmless.
 __device__ __forceinline__ int q8_encode(float x, const Q8& q) {
   const float a = __fmul_rn(fabsf(x), q.pre);
-  const float y = __fmul_rn(a, q.inv);
-  float k = fminf(floorf(__fadd_rn(y, 0.5f)), 127.f);
-  const float r_lo = __fmaf_rn(k - 0.5f, q.ss, -a);  // > 0 : k too large
-  const float r_hi = __fmaf_rn(k + 0.5f, q.ss, -a);  // <= 0: k too small
-  const bool dec = (k >= 1.f) & (r_lo > 0.f);
-  const bool inc = (k < 127.f) & (r_hi <= 0.f);
-  k = dec ? k - 1.f : (inc ? k + 1.f : k);
-  int c = q.zero ? 127 : (int)k;
+  const float y = fminf(__fmul_rn(a, q.inv), 255.f);
+  const float t = __fadd_rn(y, 8388608.f);             // 2^23 + RN(y), exact integer in the mantissa
+  const float k = fminf(__fsub_rn(t, 8388608.f), 127.f);
+  int c = min((int)(__float_as_uint(t) - 0x4B000000u), 127);
+  const float r_lo = __fmaf_rn(__fsub_rn(k, 0.5f), q.ss, -a);  // > 0 : k too large
+  const float r_hi = __fmaf_rn(__fadd_rn(k, 0.5f), q.ss, -a);  // <= 0: k too small
+  c += ((c < 127) & (r_hi <= 0.f)) - ((c >= 1) & (r_lo > 0.f));
+  c = q.zero ? 127 : c;
   c = (a == 0.f) ? 0 : c;
   return (x < 0.f) ? -c : c;
 }
-__device__ __forceinline__ float q8_decode(int code, float s) { return __fmul_rn((float)code, s); }
+// code -> exact float without I2F: the byte c + 128 under the exponent of
+// 2^23 is 2^23 + 128 + c; subtracting 2^23 + 128 is exact (and gives +0 for
+// c = 0, like the reference's f32(0) * scale)
+__device__ __forceinline__ float q8_code_float(int c) {
+  return __fsub_rn(__uint_as_float(0x4B000000u + (uint32_t)(c + 128)), 8388736.f);
+}
+__device__ __forceinline__ float q8_decode(int code, float s) { return __fmul_rn(q8_code_float(code), s); }
 
 // ----------------------------------------------------------- wire groups
 
@@ -107,12 +118,16 @@ __device__ __forceinline__ uint32_t wget(const uint4& p, int i) {
   return i == 0 ? p.x : i == 1 ? p.y : i == 2 ? p.z : p.w;
 }
 
-template <int C>
+// CHECK = false where the caller has already established finiteness (the
+// quant8 ring: pass A's block max covers every value pass B encodes)
+template <int C, bool CHECK = true>
 __device__ __forceinline__ uint4 encode_v(const FV<CodecT<C>::E>& v, const Q8& q, int& bad) {
   constexpr int E = CodecT<C>::E;
   uint32_t w[4];
+  if constexpr (CHECK) {
 #pragma unroll
-  for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
+    for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
+  }
   if constexpr (C == kNone) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) w[i] = __float_as_uint(v.v[i]);
@@ -122,9 +137,10 @@ __device__ __forceinline__ uint4 encode_v(const FV<CodecT<C>::E>& v, const Q8& q
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      uint32_t x = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) x |= ((uint32_t)(q8_encode(v.v[4 * i + k], q) & 0xFF)) << (8 * k);
+      uint32_t x;
+      const uint32_t c0 = (uint32_t)q8_encode(v.v[4 * i], q), c1 = (uint32_t)q8_encode(v.v[4 * i + 1], q);
+      const uint32_t c2 = (uint32_t)q8_encode(v.v[4 * i + 2], q), c3 = (uint32_t)q8_encode(v.v[4 * i + 3], q);
+      x = __byte_perm(__byte_perm(c0, c1, 0x0040u), __byte_perm(c2, c3, 0x0040u), 0x5410u);  // low bytes c0..c3
       w[i] = x;
     }
   }
@@ -146,7 +162,14 @@ __device__ __forceinline__ FV<CodecT<C>::E> decode_v(const uint4& p, float s) {
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v.v[i] = q8_decode((int)(int8_t)((w[i >> 2] >> (8 * (i & 3))) & 0xFF), s);
+    for (int j = 0; j < 4; ++j) {
+      // byte k of a word XOR 0x80 is code + 128; PRMT places it under the
+      // exponent pattern of 2^23 (0x4B0000xx), one FADD makes it the code
+      const uint32_t wx = w[j] ^ 0x80808080u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        v.v[4 * j + k] = __fmul_rn(__fsub_rn(__uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7440u | k)), 8388736.f), s);
+    }
   }
   return v;
 }

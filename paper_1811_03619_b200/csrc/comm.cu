@@ -81,6 +81,7 @@ struct gp_comm {
   double timeout_s = 30.0;
   gp_stats stats[kMaxRanks] = {};
   unsigned long long* trace = nullptr;  // optional device timeline buffer
+  const uint32_t* iteration_dev = nullptr;  // optional device-resident iteration tag
 };
 
 namespace {
@@ -335,6 +336,13 @@ int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
   return GP_OK;
 }
 
+int gp_comm_set_iteration_source(gp_comm* c, const uint32_t* device_tag) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  if (device_tag && (reinterpret_cast<uintptr_t>(device_tag) & 3u)) return fail(GP_ERR_ARG, "misaligned tag");
+  c->iteration_dev = device_tag;
+  return GP_OK;
+}
+
 int gp_comm_set_trace(gp_comm* c, void* device_buffer) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   c->trace = static_cast<unsigned long long*>(device_buffer);
@@ -438,6 +446,7 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
   P.pre = (flags & GP_RING_PRECOMPRESS) ? 1 : 0;
   ++c->seq;  // host-side count (info only); the kernel numbers calls on the device
   P.iteration = iteration;
+  P.iteration_dev = c->iteration_dev;
   {
     const RingPlan pl = plan_ring(n, p, c->G, codec, P.pre, c->L.ll_cap);
     P.chunk = pl.chunk;

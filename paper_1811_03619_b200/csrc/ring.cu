@@ -62,6 +62,7 @@ __shared__ uint32_t s_seq;
 __shared__ uint32_t s_bank;                 // ctl bank of this call (ring.cuh:CtlBank)
 __shared__ unsigned long long s_calls;      // raw count of calls completed before this one
 __shared__ unsigned long long s_abort;      // the abort word at kernel entry
+__shared__ uint32_t s_iter;                 // iteration tag of this call (argument or device word)
 #ifdef PIPESGD_CHECKED
 __shared__ const RingParams* s_P;           // launch parameters (bounds checks)
 #endif
@@ -209,7 +210,7 @@ __device__ bool warp_await(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrW
     if (ok && c == 0) {
       const SlotHdr* h = hdr_ptr(R.inbox, P.L, slot);
       const uint32_t hb = __ldcg(&h->block), hi = __ldcg(&h->iteration), hn = __ldcg(&h->n_elems);
-      if (hb != (uint32_t)block || hi != P.iteration || hn != (uint32_t)len) {
+      if (hb != (uint32_t)block || hi != s_iter || hn != (uint32_t)len) {
         latch_error(err, kErrHeader, phase, step, block, R.rank, (int)hn);
         broadcast_abort(P, R);
         ok = 0;
@@ -226,7 +227,7 @@ __device__ __forceinline__ void write_hdr(const RingParams& P, uint8_t* dst, int
                                           uint64_t len, float scale) {
   SlotHdr* h = hdr_ptr(dst, P.L, slot);
   h->seq = s_seq;
-  h->iteration = P.iteration;
+  h->iteration = s_iter;
   h->block = (uint32_t)block;
   h->n_elems = (uint32_t)len;
   h->scale = scale;
@@ -454,8 +455,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   Q8 q0 = q8_make(0.f);
   auto px = [&](FV<E> v) -> FV<E> {
     if (P.pre) {
+      if constexpr (C != kQuant8) {  // quant8: the whole-vector max pass already checked every x
 #pragma unroll
-      for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
+        for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
+      }
       if constexpr (C == kTrunc16) {
 #pragma unroll
         for (int i = 0; i < E; ++i) v.v[i] = t16_decode(t16_encode(v.v[i]));
@@ -492,7 +495,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   // chunk 0 carries the slot header line (collective.py:_expect, :52-64)
   auto ll_hdr_put = [&](uint8_t* llslot, uint32_t c, int block, uint64_t len, float scale) {
     if (c == 0 && lane_id() == 0)
-      ll_put(llslot, make_uint4((uint32_t)block, P.iteration, (uint32_t)len, __float_as_uint(scale)));
+      ll_put(llslot, make_uint4((uint32_t)block, s_iter, (uint32_t)len, __float_as_uint(scale)));
   };
   // warp: any lane gave up -> latch like warp_await and leave
   auto ll_ok = [&](int phase, int step, int block) -> bool {
@@ -513,7 +516,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       uint4 h;
       if (ll_get(const_cast<uint8_t*>(llslot), h, give_up)) {
         sb = h.w;
-        if (c == 0 && (h.x != (uint32_t)block || h.y != P.iteration || h.z != (uint32_t)len)) {
+        if (c == 0 && (h.x != (uint32_t)block || h.y != s_iter || h.z != (uint32_t)len)) {
           latch_error(err, kErrHeader, phase, step, block, r, (int)h.z);
           broadcast_abort(P, R);
           ok = 0;
@@ -580,7 +583,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           if (ok && c == 0) {
             const SlotHdr* h = hdr_ptr(R.inbox, P.L, rs_slot(d));
             const uint32_t hb = __ldcg(&h->block), hi = __ldcg(&h->iteration), hn = __ldcg(&h->n_elems);
-            if (hb != (uint32_t)own || hi != P.iteration || hn != (uint32_t)B.len) {
+            if (hb != (uint32_t)own || hi != s_iter || hn != (uint32_t)B.len) {
               latch_error(err, kErrHeader, kPhRS, d, own, r, (int)hn);
               broadcast_abort(P, R);
               ok = 0;
@@ -664,6 +667,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                           },
                           [&](uint64_t, uint64_t, uint64_t, int, int, const FV<E>& v) { m = max(m, absmax_bits(v)); });
           if (!warp_barrier_max(P, R, ctl, err, 0, m, vmax, 0)) return;
+          if (nonfinite(vmax)) bad = 1;  // compress() rejects the block (compression.py:108-109)
         } else {
           // one pass over the whole local vector: max|x| (pre-compress scale)
           // and max|x| over the own block, whose D(C(.)) maximum is
@@ -704,7 +708,8 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         for_groups<C>(P, B, c,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                       [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
-                        const uint4 pk = encode_v<C>(px(v), q, bad);
+                        // quant8: finiteness is known from the block max
+                        const uint4 pk = encode_v<C, C != kQuant8>(px(v), q, bad);
                         if (ll) ll_put(ll_line<C>(lld, g0 - B.A), pk);
                         else store_pay<C>(dst, g0 - B.A, vlo, vhi, pk);
                       });
@@ -826,6 +831,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         stamp(P, wid, lr, tr_step(s, 1));  // pass A done
         if (!warp_barrier_max(P, R, ctl, err, s + 1, m, vmax, s)) return;
         stamp(P, wid, lr, tr_step(s, 2));  // barrier open
+        if (nonfinite(vmax)) bad = 1;  // pass A's block max covers every value pass B encodes
         const Q8 q = q8_make(q8_scale(vmax));
         // pass B: recompute the partial, encode it with the block scale and
         // push it. Any warp may take any chunk: the chunk's flag (or LL
@@ -844,7 +850,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                         },
                         [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                           const FV<E> acc = add_v(px(v.x), decode_v<C>(v.in, sin));
-                          emit(g0, lo, hi, vlo, vhi, encode_v<C>(acc, q, bad), q.s);
+                          emit(g0, lo, hi, vlo, vhi, encode_v<C, false>(acc, q, bad), q.s);
                         });
           if (ll && !ll_ok(kPhRS, s, b)) return;
           if (!last) {
@@ -925,7 +931,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
                       if (!slot_mode) {
                         store_fv<E>(out, g0, lo, hi, decode_v<C>(v, sin));
                       } else if constexpr (C == kQuant8) {
-                        store_pay<C>(R.slot, g0, vlo, vhi, encode_v<C>(decode_v<C>(v, sin), qs, bad));
+                        store_pay<C>(R.slot, g0, vlo, vhi, encode_v<C, false>(decode_v<C>(v, sin), qs, bad));
                       } else {
                         store_pay<C>(R.slot, g0, vlo, vhi, v);
                       }
@@ -953,6 +959,11 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     s_seq = next_seq(calls);
     s_bank = (uint32_t)(calls & 1);
     s_abort = *(volatile unsigned long long*)&ctl->abort;
+    // explicit branch + asm load: a volatile dereference inside a select here
+    // built a kernel that faulted (even with a null pointer)
+    uint32_t it = P.iteration;
+    if (P.iteration_dev != nullptr) it = ld_relaxed_gpu_u32(P.iteration_dev);
+    s_iter = it;
     if (blockIdx.x % P.G == 0) {  // the next call's bank starts from zero
       CtlBank* nb = &ctl->bank[(calls + 1) & 1];
       nb->bar = 0;

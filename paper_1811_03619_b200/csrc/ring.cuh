@@ -126,6 +126,7 @@ struct RingParams {
   uint64_t n;
   uint64_t timeout_ns;
   uint32_t iteration;
+  const uint32_t* iteration_dev;  // non-null: read the tag here at kernel entry (graph replays)
   uint32_t chunk;              // elements per chunk, multiple of 8, >= kMinChunk
   int p, codec, G;             // world size, codec tag, CTAs per rank (kRingWarps warp workers each)
   int pre;                     // x is the raw gradient: apply the local D(C(.)) on load

@@ -462,9 +462,23 @@ class RankEngine:
         torch.cuda.current_stream(self.dev).synchronize()
         self.cs.synchronize()
         self.ms.synchronize()
-        if cfg.mode == MODE_D_SYNC:
-            self._capture_sync_graphs(batches, lr)
-            return
+        # the ring's iteration tag (the reference's _expect check, collective.py:52-64)
+        # is read from device memory by the captured launches; written with t
+        # before every comm replay
+        self.tag_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        if self.world > 1:
+            _lib.call("gp_comm_set_iteration_source", self.ep._comm, self.tag_dev.data_ptr())
+        try:
+            if cfg.mode == MODE_D_SYNC:
+                self._capture_sync_graphs(batches, lr)
+            else:
+                self._capture_pipe_graphs(batches, lr)
+        finally:
+            if self.world > 1:
+                _lib.call("gp_comm_set_iteration_source", self.ep._comm, None)
+
+    def _capture_pipe_graphs(self, batches, lr) -> None:
+        cfg = self.cfg
         for i in range(self.K):
             slot = self.slots[i]
             gu = torch.cuda.CUDAGraph()
@@ -531,6 +545,8 @@ class RankEngine:
         self.g_compute[i].replay()
         self.losses[t].copy_(self.static_loss[i])
         e2 = self._ev(self.cs) if tr else None
+        if self.world > 1:
+            self.tag_dev.fill_(t)
         self.g_comm[i].replay()
         if tr:
             e3 = self._ev(self.cs)
@@ -563,6 +579,8 @@ class RankEngine:
         self.ms.wait_event(self.ev_local[i])
         e1 = self._ev(self.ms) if tr else None
         with torch.cuda.stream(self.ms):
+            if self.world > 1:
+                self.tag_dev.fill_(t)
             self.g_comm[i].replay()
         self.ev_agg[i].record(self.ms)
         if tr:

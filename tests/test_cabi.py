@@ -5,6 +5,7 @@ the reference's names and pure-host semantics."""
 import ctypes
 import os
 import re
+import sys
 
 import pytest
 
@@ -148,3 +149,13 @@ def test_plain_c_client_compiles_links_and_runs(tmp_path):
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert "chunk=1024 ctas=576 ll=0 nch=2301" in r.stdout
     assert "errors ok" in r.stdout
+
+
+def test_reference_side_ctypes_shim_binds_without_a_gpu():
+    """integration/gradpipe_b200.py (the module INTEGRATION.md has the
+    reference add) binds its entry points against the built library."""
+    sys.path.insert(0, os.path.join(ROOT, "integration"))
+    import gradpipe_b200
+    L = gradpipe_b200.lib()
+    for name in ("gp_comm_create", "gp_comm_connect_local", "gp_allreduce", "gp_comm_poll_error", "gp_get_stats"):
+        assert getattr(L, name).restype is ctypes.c_int

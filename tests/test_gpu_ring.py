@@ -341,3 +341,58 @@ def test_call_over_capacity_is_a_config_error(P):
             run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, 2, ep, P.Codec.NONE))
     finally:
         tr.close()
+
+
+@multigpu
+@pytest.mark.parametrize("n", [300_007, 50_001])  # flag protocol / LL protocol
+def test_graph_replayed_ring_checks_the_device_iteration_tag(P, n):
+    """A ring captured once in a CUDA graph reads its iteration tag from
+    device memory (gp_comm_set_iteration_source), so the reference's _expect
+    check (collective.py:52-64) stays live under replay: equal tags replay
+    bit-exact, a rank one step ahead is a header error."""
+    from paper_1811_03619_b200 import _lib
+    from paper_1811_03619_b200.collective import allreduce_into
+    from paper_1811_03619_b200.engine import capture
+    p = 2
+    g = np.random.default_rng(11)
+    ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
+    want = OR.ring_allreduce_all(ins, int(P.Codec.TRUNC16)).outputs[0]
+    tr = real_transport(P, p, timeout_s=5.0, max_elems=n)
+    tags = [[7, 7], [8, 8], [9, 10]]  # the third replay: rank 1 is one iteration ahead
+
+    def op(r, ep):
+        dev = ep.device
+        with torch.cuda.device(dev):
+            x = torch.from_numpy(ins[r]).to(dev)
+            out = torch.empty_like(x)
+            tag = torch.zeros(1, dtype=torch.int32, device=dev)
+            s = torch.cuda.Stream(dev)
+            _lib.call("gp_comm_set_iteration_source", ep._comm, tag.data_ptr())
+            graph = torch.cuda.CUDAGraph()
+            with capture(graph, s):
+                allreduce_into(x, out, ep, P.Codec.TRUNC16, 0, s)
+            _lib.call("gp_comm_set_iteration_source", ep._comm, None)
+            got = []
+            for k in range(len(tags)):
+                with torch.cuda.stream(s):
+                    tag.fill_(tags[k][r])
+                    out.zero_()
+                    graph.replay()
+                s.synchronize()
+                try:
+                    ep._check_errors(n)
+                except P.CollectiveError as e:
+                    got.append(str(e))
+                    break
+                got.append(out.cpu().numpy())
+            return got
+
+    try:
+        res = run_ranks(tr, op)
+    finally:
+        tr.close()
+    for r in range(p):
+        assert len(res[r]) == 3, res[r]
+        for k in range(2):
+            assert_bits_equal(res[r][k], want, f"rank {r} replay {k}")
+    assert any(isinstance(x, str) and "iteration tag" in x for x in (res[0][2], res[1][2])), (res[0][2], res[1][2])
