@@ -528,8 +528,9 @@ def our_arm(args, ws, rank, local):
             step(t)
             t += 1
         copy_events.clear()
-        e2e_ms, _ = timed_region(t, args.steps, e2e=True)
+        e2e_ms, e2e_events = timed_region(t, args.steps, e2e=True)
         copy_ms = [a.elapsed_time(b) for a, b in copy_events]
+        streams = stream_timeline(e2e_events, copy_events)
         t += args.steps
         if use_graphs:
             eng.drain_graph(t - 1)
@@ -659,6 +660,16 @@ def our_arm(args, ws, rank, local):
             store.wait(["pipesgd_eq5_calibration"])
         torch.cuda.synchronize(dev)
 
+    # Eq. 5's gamma (one fused hop on this GPU over a block of n/p) and S
+    # (all-rank GPU barrier), measured directly rather than fitted from the ring
+    probes = None
+    if N > 1 and not args.no_allreduce_sweep:
+        from paper_1811_03619_b200 import timing as T
+        S = max_over_ranks(T.barrier_time(ep), dev)
+        probes = {"S_s": S, "gamma_s_per_byte": T.gamma_hop(args.codec, max(1, n // N), dev) if rank == 0 else None,
+                  "gamma_s_per_byte_1k": T.gamma_hop(args.codec, max(1, 1024 // N), dev) if rank == 0 else None,
+                  "gamma_s_per_byte_big": T.gamma_hop(args.codec, (1 << 26) // N, dev) if rank == 0 else None}
+
     line = None
     if rank == 0:
         h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
@@ -670,6 +681,7 @@ def our_arm(args, ws, rank, local):
                 "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d * N,
                         "d2h_bytes_per_step": 4 * N,
                         "h2d_copy_ms_avg": float(np.mean(copy_ms)) if copy_ms else None,
+                        "streams": streams,
                         "how": "same engine; every step copies the rank's batch from pinned host memory (on a "
                                "copy stream into a per-parity buffer, overlapping the previous step's compute) "
                                "and reads its loss back into pinned memory (on a D2H stream after the step)"},
@@ -692,8 +704,45 @@ def our_arm(args, ws, rank, local):
                 "codec_none_frac": none_gbs / NVLINK_PEAK_GBS if none_gbs else None,
                 "note": "the same ring kernel alone on a 256 MiB fp32 bucket with every SM (standalone "
                         "allreduce configuration); the engine runs it on %d CTAs beside the CNN" % args.ctas}
-        line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms, calib)
+        line["timing_model"] = timing_model(avg, iso, n, N, w, allreduce, args.codec, per_step_ms, calib, probes,
+                                            args.mode, args.depth, args.steps)
     return line
+
+
+def stream_timeline(events, copies):
+    """Per-step stream timeline of the end-to-end region from the engine's
+    CUDA events: gaps on the compute stream between consecutive steps, the
+    comm kernel's start relative to its step's compute end, and whether the
+    batch copy was still running when the step that reads it started."""
+    if not events:
+        return None
+    t0 = events[0][2]
+    by = {}
+    for (t, stage, e0, e1, _) in events:
+        by.setdefault(t, {})[stage] = (t0.elapsed_time(e0), t0.elapsed_time(e1))
+    steps = sorted(by)
+    gaps, comm_lag, comm_ms, compute_ms = [], [], [], []
+    for a_, b_ in zip(steps, steps[1:]):
+        if "backward" in by[a_] and "update" in by[b_]:
+            gaps.append(by[b_]["update"][0] - by[a_]["backward"][1])
+    for t in steps:
+        st = by[t]
+        if "backward" in st:
+            compute_ms.append(st["backward"][1] - st["backward"][0])
+        if "allreduce" in st and "backward" in st:
+            comm_lag.append(st["allreduce"][0] - st["backward"][1])
+            comm_ms.append(st["allreduce"][1] - st["allreduce"][0])
+    late = []
+    for i, (c0, c1) in enumerate(copies[1:], start=1):  # copy i feeds step steps[i]
+        if i < len(steps) and "update" in by[steps[i]]:
+            late.append(t0.elapsed_time(c1) - by[steps[i]]["update"][0])
+    f = lambda v: float(np.mean(v)) if v else None  # noqa: E731
+    return {"compute_gap_ms_avg": f(gaps), "compute_ms_avg": f(compute_ms), "comm_ms_avg": f(comm_ms),
+            "comm_start_after_compute_ms_avg": f(comm_lag),
+            "copy_end_minus_step_start_ms_avg": f(late),
+            "note": "events on the compute / comm streams (engine trace) and the copy stream; a positive "
+                    "copy_end_minus_step_start means the copy ended after the step that reads it started "
+                    "(the compute graph then waits on it)"}
 
 
 def ncu_traffic():
@@ -833,14 +882,21 @@ def ring_vs_nccl(ep, codec, N, dev, sizes, ctas_list=(0,)):
     return out
 
 
-def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None):
-    """The paper's timing model (timing.py:97-132, harness.py:667-720) with
-    GPU-measured symbols. Ring: Eq. 5 T = 2(p-1)a + 2(p-1)/p n b (+ n g + S
-    folded into a: the fused kernel overlaps its reduction with the transfer),
-    with a and b fitted like the reference's calibrate() (ping + flood) from
-    the ring itself at a 4 KiB and a 256 MiB bucket; prediction for the step's
-    gradient vs the measured isolated ring. Iteration: Eq. 4 (pipe) / Eq. 2
-    (sync) from the measured stage times vs the measured step."""
+def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probes=None, mode="pipe_sgd",
+                 depth=2, steps=30):
+    """The paper's timing model with GPU-measured symbols (timing.py:97-132,
+    harness.py:513-720).
+
+    * Eq. 4 (pipe) / Eq. 2 (sync) from the stage times measured inside the
+      step (update, compute, in-pipeline comm) vs the measured step.
+    * Eq. 5 for the ring: alpha = one-way flag latency (gp_calib_pingpong),
+      beta = bidirectional peer push per byte (gp_calib_p2p_copy), gamma =
+      one fused hop C(x + D(in)) on one GPU per payload byte (gp_calib_hop,
+      the reference's reduce_hop), S = an all-rank GPU barrier
+      (gp_comm_barrier, the reference's barrier probe); each ring size of the
+      allreduce rows is compared with its Eq. 5 prediction (25 % flag).
+    * compare_prediction (harness.py:687-720): the iteration predicted with
+      Eq. 5's comm (predict_iteration_time, harness.py:667-684) vs measured."""
     from paper_1811_03619_b200 import timing as T
     upd = avg.get("update", 0.0) + avg.get("compress", 0.0)
     comp = avg.get("backward", 0.0)
@@ -852,40 +908,32 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None):
     out["measured_step_ms"] = step_ms
     out["eq4_over_measured"] = out["eq4_pipe_ms"] / step_ms
     out["bound"] = "compute" if upd + comp >= comm else "communication"
-    if allreduce and N > 1:
-        small, big = allreduce[0], allreduce[-1]
-        wb = lambda m: 2 * (N - 1) / N * m * w  # wire bytes per rank
-        t_small, t_big = small[codec]["ms"] * 1e-3, big[codec]["ms"] * 1e-3
-        beta = (t_big - t_small) / (wb(big["n"]) - wb(small["n"]))
-        alpha = max(0.0, (t_small - wb(small["n"]) * beta) / (2 * (N - 1)))
-        params = T.ClusterParams(workers=N, latency_s=alpha, byte_time_s=beta / 2, model_bytes=n * w)
-        pred = T.ring_comm_time(params)  # 2(p-1)/p * n * (beta/2) * 2 == wire bytes * beta
-        mid = allreduce[1]
-        meas = mid[codec]["ms"] * 1e-3  # same back-to-back method as the calibration points
-        out.update({"alpha_us": alpha * 1e6, "beta_gbs": 1 / beta / 1e9 if beta > 0 else None,
-                    "eq5_ring_pred_ms": pred * 1e3, "ring_measured_ms": meas * 1e3,
-                    "ring_isolated_barrier_aligned_ms": iso.get("ring"),
-                    "eq5_over_measured": pred / meas if meas else None,
-                    "within_25pct": bool(meas and abs(pred / meas - 1) <= 0.25)})
-        if calib:
-            # SURVEY 8(d) form: T = 2(p-1) a + 2(p-1)/p nb b + (p-1)/p nb g + S with
-            # a = one-way flag latency (gp_calib_pingpong), b = bidirectional peer
-            # push (gp_calib_p2p_copy), g = the codec's D(C(.)) pass per payload
-            # byte on one GPU, S = the 4 KiB ring's time beyond its 2(p-1) flag hops
-            a, b = max(0.0, calib["alpha_s"]), calib["beta_s_per_byte"]
-            nb = n * w
-            g = (iso["roundtrip"] * 1e-3 / nb) if iso.get("roundtrip") else 0.0
-            S = max(0.0, t_small - 2 * (N - 1) * a)
-            terms = {"latency": 2 * (N - 1) * a, "bandwidth": 2 * (N - 1) / N * nb * b,
-                     "reduction": (N - 1) / N * nb * g, "fixed": S}
-            pc = sum(terms.values())
-            out["eq5_calibrated"] = {
-                "alpha_us": a * 1e6, "beta_push_gbs": calib["push_gbs"], "gamma_gbs": 1 / g / 1e9 if g else None,
-                "S_us": S * 1e6, "terms_us": {k: v * 1e6 for k, v in terms.items()},
-                "pred_ms": pc * 1e3, "ring_measured_ms": meas * 1e3, "pred_over_measured": pc / meas if meas else None,
-                "note": "the paper's model assumes one pipelined transfer per hop; the fused ring overlaps the "
-                        "reduction with the transfer (gamma term pessimistic) but pays a fence-bounded phase "
-                        "ramp at this size (profiles/r01_ring_latency)"}
+    if not (allreduce and N > 1 and calib and probes):
+        return out
+    a, b, S = max(0.0, calib["alpha_s"]), calib["beta_s_per_byte"], probes["S_s"]
+    rows = []
+    for row, g in zip(allreduce, ("gamma_s_per_byte_1k", "gamma_s_per_byte", "gamma_s_per_byte_big")):
+        gam = probes.get(g) or 0.0
+        rows.append(T.compare_ring(row[codec]["ms"] * 1e-3, N, codec, row["n"], a, b, gam, S))
+    mid = rows[1]
+    gam = probes["gamma_s_per_byte"] or 0.0
+    cluster = T.ClusterParams(workers=N, latency_s=a, byte_time_s=b, reduce_time_s=gam, sync_time_s=S,
+                              model_bytes=float(n * w))
+    pred_it = T.predict_iteration_time(T.StageTimes(update=upd / 1e3, forward=0.0, backward=comp / 1e3,
+                                                    comm=T.ring_comm_time(cluster)),
+                                       cluster, "d_sync" if mode == "d_sync" else "pipe_sgd", steps, depth)
+    rel = (step_ms * 1e-3 - pred_it) / pred_it
+    out["eq5"] = {
+        "symbols": {"alpha_us": a * 1e6, "beta_push_gbs": calib["push_gbs"],
+                    "gamma_gbs": 1 / gam / 1e9 if gam else None, "S_us": S * 1e6},
+        "rings": rows, "step_gradient_ring": mid,
+        "note": "measured = the same ring alone, back-to-back (the allreduce rows); Eq. 5 adds the fused hop's "
+                "compute serially although the kernel overlaps it with the transfer, and has no per-hop "
+                "phase ramp"}
+    out["compare_prediction"] = [{"mode": mode, "measured_ms": step_ms, "predicted_ms": pred_it * 1e3,
+                                  "rel_error": rel, "flagged": abs(rel) > 0.25,
+                                  "bound": "communication" if T.ring_comm_time(cluster) > (upd + comp) / 1e3
+                                  else "compute"}]
     return out
 
 

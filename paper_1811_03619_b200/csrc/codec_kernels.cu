@@ -171,6 +171,48 @@ __global__ void __launch_bounds__(kT, PIPESGD_CU_MINB) consume_update_kernel(flo
                    });
 }
 
+// One reduce-scatter hop on one GPU (the timing model's gamma, the
+// reference calibrate()'s reduce_hop: compress(decompress(block) + grad),
+// harness.py:561-568): acc = x + D(in); pass 1 (quant8) max|acc|, pass 2
+// out = C(acc) with that block scale. No NVLink: the hop's compute and HBM
+// share, per payload byte.
+template <int C>
+__global__ void __launch_bounds__(kT) hop_absmax_kernel(const float* __restrict__ x, const uint8_t* in,
+                                                        const float* in_scale, uint64_t n, gp_codec_status* st) {
+  constexpr int E = CodecT<C>::E;
+  __shared__ uint32_t red[kT / 32];
+  const float s = (C == kQuant8) ? *in_scale : 0.f;
+  uint32_t m = 0;
+  struct XI {
+    FV<E> x;
+    uint4 in;
+  };
+  stream_groups<E>(n, [&](uint64_t g0) { return XI{load_fv<E>(x, g0, 0, n), load_pay<C>(in, g0, 0, (int)(min(n, g0 + E) - g0))}; },
+                   [&](uint64_t, const XI& v) { m = max(m, absmax_bits(add_v(v.x, decode_v<C>(v.in, s)))); });
+  m = cta_max_u32<kT>(m, red);
+  if (threadIdx.x == 0) atomicMax(&st->absmax_bits, m);
+}
+
+template <int C>
+__global__ void __launch_bounds__(kT) hop_encode_kernel(const float* __restrict__ x, const uint8_t* in,
+                                                        const float* in_scale, uint64_t n, uint8_t* out,
+                                                        gp_codec_status* st) {
+  constexpr int E = CodecT<C>::E;
+  const float s = (C == kQuant8) ? *in_scale : 0.f;
+  const Q8 q = status_scale<C>(st);
+  int bad = 0;
+  struct XI {
+    FV<E> x;
+    uint4 in;
+  };
+  stream_groups<E>(n, [&](uint64_t g0) { return XI{load_fv<E>(x, g0, 0, n), load_pay<C>(in, g0, 0, (int)(min(n, g0 + E) - g0))}; },
+                   [&](uint64_t g0, const XI& v) {
+                     store_pay<C>(out, g0, 0, (int)(min(n, g0 + E) - g0),
+                                  encode_v<C>(add_v(v.x, decode_v<C>(v.in, s)), q, bad));
+                   });
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
+}
+
 int cfail(int code, const std::string& m) {
   gp_set_error_string(m);
   return code;
@@ -266,6 +308,31 @@ static int consume_update(float* w, int codec, const void* slot, const float* sc
 int gp_consume_update(float* w, int codec, const void* slot, const float* scale, uint64_t n, float lr,
                       int world, void* stream) {
   return consume_update(w, codec, slot, scale, n, lr, nullptr, world, stream);
+}
+
+int gp_calib_hop(int codec, const float* x, const void* in, const float* in_scale, void* out, uint64_t n,
+                 gp_codec_status* st, void* stream) {
+  if (codec < 0 || codec > 2) return cfail(GP_ERR_ARG, "unknown codec");
+  if (!st) return cfail(GP_ERR_ARG, "null status");
+  if (n && (!x || !in || !out)) return cfail(GP_ERR_ARG, "null buffer");
+  if (n && codec == kQuant8 && !in_scale) return cfail(GP_ERR_ARG, "quant8 hop needs the incoming scale");
+  if (n && (mis(x) || mis(in) || mis(out))) return cfail(GP_ERR_ARG, "buffers must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(st, 0, sizeof(*st), s);
+  if (e != cudaSuccess) return cfail(GP_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+  if (n == 0) return GP_OK;
+  const uint32_t g = grid_for(n);
+  auto* pi = static_cast<const uint8_t*>(in);
+  auto* po = static_cast<uint8_t*>(out);
+  if (codec == kQuant8) {
+    hop_absmax_kernel<kQuant8><<<g, kT, 0, s>>>(x, pi, in_scale, n, st);
+    hop_encode_kernel<kQuant8><<<g, kT, 0, s>>>(x, pi, in_scale, n, po, st);
+  } else if (codec == kTrunc16) {
+    hop_encode_kernel<kTrunc16><<<g, kT, 0, s>>>(x, pi, in_scale, n, po, st);
+  } else {
+    hop_encode_kernel<kNone><<<g, kT, 0, s>>>(x, pi, in_scale, n, po, st);
+  }
+  return check_launch("hop kernel");
 }
 
 int gp_consume_update_dev(float* w, int codec, const void* slot, const float* scale, uint64_t n,

@@ -82,6 +82,7 @@ struct gp_comm {
   gp_stats stats[kMaxRanks] = {};
   unsigned long long* trace = nullptr;  // optional device timeline buffer
   const uint32_t* iteration_dev = nullptr;  // optional device-resident iteration tag
+  uint64_t bar_gen = 0;                 // gp_comm_barrier generations issued
 };
 
 namespace {
@@ -398,6 +399,35 @@ int gp_comm_destroy(gp_comm* c) {
   return GP_OK;
 }
 
+// All-to-all flag barrier over NVSwitch, `rounds` times (the timing model's
+// S, the reference's barrier probe harness.py:589-609): one thread per rank
+// publishes generation g to every peer's ctl and waits until every peer's
+// generation reached g. Writes the elapsed %globaltimer ns to ns_out.
+struct PeerTable {
+  uint8_t* peer[kMaxRanks];
+};
+
+__global__ void barrier_kernel(const __grid_constant__ PeerTable T, uint64_t off_ctl, int p, int rank, uint64_t base,
+                               int rounds, uint64_t timeout_ns, unsigned long long* ns_out) {
+  Ctl* mine = reinterpret_cast<Ctl*>(T.peer[rank] + off_ctl);
+  const uint64_t t0 = globaltimer();
+  for (int k = 1; k <= rounds; ++k) {
+    const unsigned long long g = base + k;
+    for (int q = 0; q < p; ++q)
+      if (q != rank) st_release_sys(reinterpret_cast<uint64_t*>(&reinterpret_cast<Ctl*>(T.peer[q] + off_ctl)->barflag[rank]), g);
+    for (int q = 0; q < p; ++q) {
+      if (q == rank) continue;
+      while (ld_acquire_sys(reinterpret_cast<const uint64_t*>(&mine->barflag[q])) < g) {
+        if (globaltimer() - t0 > timeout_ns) {
+          *ns_out = ~0ull;
+          return;
+        }
+      }
+    }
+  }
+  *ns_out = globaltimer() - t0;
+}
+
 __global__ void status_to_error_kernel(const gp_codec_status* st, ErrWord* e, int rank) {
   if (st->nonfinite) latch_error(e, kErrNonFinite, kPhRS, 0, rank, rank, 0);
 }
@@ -605,6 +635,20 @@ int gp_broadcast_emulated(gp_comm* c, const float* const* ins, float* const* out
   if (!c || (c->nlocal == 1 && c->world > 1)) return fail(GP_ERR_STATE, "not an emulated communicator");
   DeviceGuard g(c->device);
   return star(c, ins, outs, n, root, 1, 0, static_cast<cudaStream_t>(stream));
+}
+
+int gp_comm_barrier(gp_comm* c, int rounds, void* ns_out, void* stream) {
+  if (!c || !ns_out || rounds < 1) return fail(GP_ERR_ARG, "barrier needs a communicator, rounds >= 1, ns_out");
+  if (c->nlocal != 1 || !c->connected) return fail(GP_ERR_STATE, "not a connected per-rank communicator");
+  DeviceGuard g(c->device);
+  PeerTable T{};
+  for (int q = 0; q < kMaxRanks; ++q) T.peer[q] = c->peer[q];
+  barrier_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      T, c->L.off_ctl, c->world, c->rank, c->bar_gen, rounds, (uint64_t)(c->timeout_s * 1e9),
+      static_cast<unsigned long long*>(ns_out));
+  c->bar_gen += (uint64_t)rounds;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GP_OK : cuda_fail(e, "barrier kernel launch");
 }
 
 int gp_comm_poll_error(gp_comm* c, gp_error* out) {

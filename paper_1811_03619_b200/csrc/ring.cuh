@@ -19,7 +19,8 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 // Low-latency (LL) protocol for small blocks: every 8-byte word carries 4
 // payload bytes and the call's sequence number, so a receiver polls the data
 // itself and no release fence / flag store is needed, at twice the bytes.
-// A none/trunc16 call takes it when its block payload (elements incl. the
+// A call of any codec takes it (quant8's block scale rides in the header
+// line's fourth word) when its block payload (elements incl. the
 // 16-element alignment slack x wire width) is at most kLLHopBytes x (p - 1):
 // every further hop saves one more fence (measured crossover: 512 KB at
 // p = 2, >= 1 MB at p = 4; profiles/r01_c5/ll_threshold_ab.log). Compile-time
@@ -64,6 +65,7 @@ struct Ctl {                   // rank-private control block (peers write abort 
   unsigned long long abort;    // kAbortSticky | rank + 1 | seq of the call that failed (0 = healthy)
   CtlBank bank[2];
   unsigned long long ack[kMaxRanks];  // star calls: == seq once rank q consumed this rank's data
+  unsigned long long barflag[kMaxRanks];  // gp_comm_barrier: generation rank q reached (written by q)
 };
 static_assert(sizeof(Ctl) <= 2048, "ctl block: the p = 1 codec status lives at +2048");
 

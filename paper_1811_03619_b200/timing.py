@@ -217,3 +217,87 @@ def calibrate_nvlink(devices=(0, 1), nbytes: int = 1 << 30, ctas: int = 148, ite
         raise RuntimeError("flag ping-pong timed out (is the peer GPU busy with another process?)")
     alpha = t / iters / 2 / 1e9
     return {"alpha_s": alpha, "beta_s_per_byte": beta, "push_gbs": 1 / beta / 1e9}
+
+
+def gamma_hop(codec, n: int, device, reps: int = 10) -> float:
+    """Eq. 5's gamma on this GPU: seconds per payload byte of one fused
+    reduce-scatter hop out = C(x + D(in)) over an n-element block (the
+    reference calibrate()'s reduce_hop, harness.py:561-568), inputs cold in L2
+    (a 256 MiB read between launches, subtracted)."""
+    import torch
+
+    from . import _lib
+    from .compression import CodecStatus, as_codec, encode_async
+
+    codec = as_codec(codec)
+    w = codec.bytes_per_elem
+    with torch.cuda.device(device):
+        s = torch.cuda.Stream(device)
+        x = torch.randn(n, device=device) * 1e-2
+        pay = torch.empty(max(16, n * w), dtype=torch.uint8, device=device)
+        out = torch.empty_like(pay)
+        st_in, st = CodecStatus(torch.device(device)), CodecStatus(torch.device(device))
+        flush = torch.ones(64 << 20, dtype=torch.float32, device=device)
+        with torch.cuda.stream(s):
+            encode_async(x, codec, pay, st_in, s.cuda_stream)
+
+        def series(hop: bool) -> float:
+            s.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                flush.sum()
+                torch.cuda._sleep(2_000_000)
+                a.record(s)
+                for _ in range(reps):
+                    flush.sum()
+                    if hop:
+                        _lib.call("gp_calib_hop", int(codec), x.data_ptr(), pay.data_ptr(), st_in.scale_view.data_ptr(),
+                                  out.data_ptr(), n, st.ptr, s.cuda_stream)
+                b.record(s)
+            b.synchronize()
+            return a.elapsed_time(b) / 1e3
+
+        series(True)
+        t = max(0.0, (series(True) - series(False)) / reps)
+    return t / max(1, n * w)
+
+
+def barrier_time(endpoint, rounds: int = 200) -> float:
+    """Eq. 5's S on the GPUs: one all-to-all flag barrier over the
+    communicator (gp_comm_barrier; the reference's barrier probe,
+    harness.py:589-609), seconds per barrier. Every rank must call it."""
+    import torch
+
+    from . import _lib
+
+    dev = endpoint.device
+    with torch.cuda.device(dev):
+        s = torch.cuda.Stream(dev)
+        ns = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.call("gp_comm_barrier", endpoint._comm, 8, ns.data_ptr(), s.cuda_stream)  # warm-up
+        s.synchronize()
+        _lib.call("gp_comm_barrier", endpoint._comm, int(rounds), ns.data_ptr(), s.cuda_stream)
+        s.synchronize()
+        t = int(ns.item())
+    if t < 0 or t == (1 << 64) - 1:
+        raise RuntimeError("GPU barrier probe timed out")
+    return t / 1e9 / rounds
+
+
+def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: float, gamma: float, sync: float,
+                 flag_threshold: float = 0.25) -> dict:
+    """One prediction-vs-measurement row for a ring call (compare_prediction,
+    harness.py:687-720, applied to Eq. 5 itself): n is the element count,
+    model bytes are the codec's payload (harness.py:562)."""
+    from .compression import as_codec
+
+    nb = float(n * as_codec(codec).bytes_per_elem)
+    params = ClusterParams(workers=p, latency_s=alpha, byte_time_s=beta, reduce_time_s=gamma, sync_time_s=sync,
+                           model_bytes=nb)
+    lat, bw, red, syn = _ring_terms(params, 1)
+    pred = ring_comm_time(params)
+    rel = (measured_s - pred) / pred if pred > 0 else float("inf")
+    return {"n": n, "codec": as_codec(codec).name.lower(), "measured_ms": measured_s * 1e3, "eq5_ms": pred * 1e3,
+            "terms_us": {"latency": lat * 1e6, "bandwidth": bw * 1e6, "reduction": red * 1e6, "sync": syn * 1e6},
+            "eq5_over_measured": pred / measured_s if measured_s > 0 else None, "rel_error": rel,
+            "flagged": abs(rel) > flag_threshold}

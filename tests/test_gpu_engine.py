@@ -240,3 +240,24 @@ def test_star_back_to_back_over_nvlink_across_sequence_wrap(P):
                 assert o.tobytes() == value.tobytes()
     finally:
         tr.close()
+
+
+def test_c1_mnist_mlp_torch_gradients_within_tolerance(P):
+    """C1 at its real shape (BASELINE configs[0]): MLP 784-500-500-10
+    (648,010 params), p = 4, codec none, Pipe-SGD width 2, batch 25 per rank,
+    gradients from torch on the GPU (fp32) against the oracle trajectory
+    (numpy, the reference's math). Tolerance after 10 steps: rtol 1e-4 and
+    atol 1e-5 x max|w| (fp32 GEMM summation order differs from numpy's)."""
+    from paper_1811_03619_b200.engine import RunConfig, run_inproc_cluster
+    from paper_1811_03619_b200.models import ModelSpec
+    data = OE.synthetic_blobs(dim=784, num_classes=10, num_samples=2000, seed=0)
+    p, T = 4, 10
+    cfg = RunConfig(mode="pipe_sgd", iterations=T, learning_rate=0.05, codec="none", depth=2, batch_size=25, seed=0)
+    res = run_inproc_cluster(p, cfg, data, ModelSpec("mlp", (784, 500, 500, 10)))
+    want = OE.run_trajectory(p, OE.Config(mode="pipe_sgd", iterations=T, learning_rate=0.05, codec=0, batch_size=25,
+                                          seed=0), data, OE.Net("mlp", (784, 500, 500, 10))).params
+    assert res[0].params.size == 648_010
+    for r in res:
+        np.testing.assert_allclose(r.params, want, rtol=1e-4, atol=1e-5 * max(1.0, np.abs(want).max()))
+    for r in res[1:]:
+        assert_bits_equal(r.params, res[0].params, "replicas diverged")
