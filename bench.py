@@ -589,9 +589,11 @@ def our_arm(args, ws, rank, local):
         roof = {"kernel": "ring_allreduce_kernel<%s> (fused decode+add+encode+NVLink push)" % args.codec,
                 "bound": "nvlink", "achieved": live, "peak": NVLINK_PEAK_GBS,
                 "unit": "GB/s", "frac": live / NVLINK_PEAK_GBS,
-                "traffic": None,
-                "traffic_note": "ncu cannot profile the multi-process ring; the emulated capture in "
-                                "profiles/r01_final/ncu_summary.md has its HBM traffic",
+                "traffic": traffic.get(f"ring_{args.codec}_fused_p{N}_n{n}"),
+                "traffic_note": "ncu cannot replay the multi-process ring (its ranks wait on each other); traffic "
+                                "is the DRAM bytes per rank of the same fused ring with all ranks emulated in one "
+                                "launch (profiles/ncu_traffic.json), null when no capture exists for this "
+                                "(codec, p, n)",
                 "measured": "CUDA events on the comm stream around every ring launch of the timed region "
                             "(the launch shares the SMs with the CNN and waits for the slower rank); the same "
                             "kernel alone (20 back-to-back launches after L2-evicting reads, minus the reads): "
@@ -666,9 +668,12 @@ def our_arm(args, ws, rank, local):
     if N > 1 and not args.no_allreduce_sweep:
         from paper_1811_03619_b200 import timing as T
         S = max_over_ranks(T.barrier_time(ep), dev)
-        probes = {"S_s": S, "gamma_s_per_byte": T.gamma_hop(args.codec, max(1, n // N), dev) if rank == 0 else None,
-                  "gamma_s_per_byte_1k": T.gamma_hop(args.codec, max(1, 1024 // N), dev) if rank == 0 else None,
-                  "gamma_s_per_byte_big": T.gamma_hop(args.codec, (1 << 26) // N, dev) if rank == 0 else None}
+        g = ep.info()["ctas"]  # the probes run on the ring's own thread budget
+        probes = {"S_s": S}
+        if rank == 0:
+            for key, m in (("1k", 1024), ("mid", n), ("big", 1 << 26)):
+                probes["gamma_" + key] = T.gamma_hop(args.codec, max(1, m // N), dev, ring_ctas=g)
+                probes["delta_" + key] = T.delta_decode(args.codec, max(1, m // N), dev)
 
     line = None
     if rank == 0:
@@ -912,11 +917,11 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
         return out
     a, b, S = max(0.0, calib["alpha_s"]), calib["beta_s_per_byte"], probes["S_s"]
     rows = []
-    for row, g in zip(allreduce, ("gamma_s_per_byte_1k", "gamma_s_per_byte", "gamma_s_per_byte_big")):
-        gam = probes.get(g) or 0.0
-        rows.append(T.compare_ring(row[codec]["ms"] * 1e-3, N, codec, row["n"], a, b, gam, S))
+    for row, key in zip(allreduce, ("1k", "mid", "big")):
+        rows.append(T.compare_ring(row[codec]["ms"] * 1e-3, N, codec, row["n"], a, b, probes["gamma_" + key], S,
+                                   probes["delta_" + key]))
     mid = rows[1]
-    gam = probes["gamma_s_per_byte"] or 0.0
+    gam = probes["gamma_mid"]
     cluster = T.ClusterParams(workers=N, latency_s=a, byte_time_s=b, reduce_time_s=gam, sync_time_s=S,
                               model_bytes=float(n * w))
     pred_it = T.predict_iteration_time(T.StageTimes(update=upd / 1e3, forward=0.0, backward=comp / 1e3,
@@ -927,9 +932,9 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
         "symbols": {"alpha_us": a * 1e6, "beta_push_gbs": calib["push_gbs"],
                     "gamma_gbs": 1 / gam / 1e9 if gam else None, "S_us": S * 1e6},
         "rings": rows, "step_gradient_ring": mid,
-        "note": "measured = the same ring alone, back-to-back (the allreduce rows); Eq. 5 adds the fused hop's "
-                "compute serially although the kernel overlaps it with the transfer, and has no per-hop "
-                "phase ramp"}
+        "note": "measured = the same ring alone, back-to-back, at the engine's CTA budget (the allreduce rows); "
+                "gamma is one fused hop on one GPU on that same budget; eq5_ext adds the step-0 encode and the "
+                "allgather decode the paper's model leaves out (timing.compare_ring)"}
     out["compare_prediction"] = [{"mode": mode, "measured_ms": step_ms, "predicted_ms": pred_it * 1e3,
                                   "rel_error": rel, "flagged": abs(rel) > 0.25,
                                   "bound": "communication" if T.ring_comm_time(cluster) > (upd + comp) / 1e3

@@ -178,14 +178,20 @@ int gp_calib_p2p_copy_ex(void* dst, const void* src, uint64_t bytes, int ctas, i
                          void* counter /* device u64, zeroed */, void* flags /* device u64[] */, void* stream);
 /* One reduce-scatter hop on one GPU for the timing model's gamma (the
  * reference calibrate()'s reduce_hop, harness.py:561-568): out = C(x + D(in))
- * with the block scale of the sum (quant8: two passes), scale into st. */
+ * with the block scale of the sum (quant8: two passes), scale into st; `grid`
+ * lets the probe run on the ring's own thread budget. */
 int gp_calib_hop(int codec, const float* x, const void* in, const float* in_scale, void* out, uint64_t n,
-                 gp_codec_status* st, void* stream);
+                 int grid /* CTAs of 256 threads; 0 = fill the GPU */, gp_codec_status* st, void* stream);
 /* All-to-all flag barrier across the communicator's ranks, `rounds` times in
  * one launch (the timing model's S, the reference barrier probe
  * harness.py:589-609); every rank must call it; elapsed ns -> ns_out (device
  * u64, ~0 on timeout). */
 int gp_comm_barrier(gp_comm* comm, int rounds, void* ns_out, void* stream);
+/* Bounds-checked build (libpipesgd_checked.so) only: payload bytes the ring
+ * kernels of `rank` stored into other ranks' inboxes since the last reset --
+ * the bytes a multi-GPU run moves over NVLink, counted by the kernel itself.
+ * Always 0 in the product build. */
+int gp_comm_wire_bytes(gp_comm* comm, int rank, int reset, uint64_t* out);
 int gp_calib_pingpong(void* mine, void* theirs, int iters, int initiator, uint64_t base,
                       void* ns_out /* device u64 */, void* stream);
 

@@ -9,7 +9,7 @@ Python package); torch only allocates device buffers and streams.
     gradpipe.engine.run_inproc_cluster(...)   # the reference's own loop, B200 ring underneath
     undo()
 
-install() swaps two names the reference's engine resolves at call time:
+install() swaps the names the reference's engine resolves at call time:
   * gradpipe.engine.InProcTransport (engine.py:49, :582) -> B200Transport:
     same constructor (world_size, latency_s, byte_time_s, timeout_s) and
     endpoint surface (rank, world_size, timeout_s, latency_s, byte_time_s,
@@ -18,7 +18,9 @@ install() swaps two names the reference's engine resolves at call time:
   * gradpipe.engine.ring_allreduce / gradpipe.collective.ring_allreduce
     (engine.py:354-361, :399-406 -> collective.py:143-163) -> a wrapper that
     sends B200 endpoints to gp_allreduce and every other endpoint to the
-    original function.
+    original function;
+  * gradpipe.engine.barrier (engine.py:454, the run-start barrier;
+    collective.py:283-297) -> gp_comm_barrier for B200 endpoints.
 Everything else -- codecs, the pipelined loop, GradientBuffer, SGD -- stays
 the reference's own numpy code, so the run's final weights must equal a
 plain reference run bit for bit (tests/test_gpu_integration.py).
@@ -59,6 +61,7 @@ def lib():
             "gp_comm_set_tuning": [_vp, _i, _d],
             "gp_allreduce": [_vp, _vp, _vp, _u64, _i, _u32, _vp],
             "gp_comm_poll_error": [_vp, ctypes.POINTER(_Error)],
+            "gp_comm_barrier": [_vp, _i, _vp, _vp],
             "gp_get_stats": [_vp, _i, ctypes.POINTER(_Stats)],
             "gp_comm_destroy": [_vp],
             "gp_last_error_string": [],
@@ -170,6 +173,21 @@ def ring_allreduce_b200(local, rank, p, endpoint, codec, iteration=0):
         return out.cpu().numpy()
 
 
+def barrier_b200(rank, p, endpoint):
+    """collective.py:283-297 through gp_comm_barrier (all-to-all flag barrier
+    over the GPUs): no rank returns before all have entered."""
+    import torch
+    from gradpipe.errors import CollectiveError
+    if endpoint.rank != rank or endpoint.world_size != p:
+        raise CollectiveError("endpoint does not match caller's rank/size")
+    with torch.cuda.device(endpoint.device):
+        ns = torch.zeros(1, dtype=torch.int64, device=endpoint.device)
+        _check(lib().gp_comm_barrier(endpoint.comm, 1, ns.data_ptr(), endpoint.stream.cuda_stream), "gp_comm_barrier")
+        endpoint.stream.synchronize()
+        if int(ns.item()) == -1:
+            raise CollectiveError(f"barrier (rank {rank}): timed out after {endpoint.timeout_s:g}s")
+
+
 def install(gradpipe):
     """Route the reference engine's ring through the B200 C ABI; returns undo()."""
     import gradpipe.collective as C
@@ -188,12 +206,21 @@ def install(gradpipe):
         live.append(tr)
         return tr
 
+    orig_barrier = E.barrier
+
+    def barrier(rank, p, endpoint, generation=0):
+        if isinstance(endpoint, B200Endpoint):
+            return barrier_b200(rank, p, endpoint)
+        return orig_barrier(rank, p, endpoint, generation)
+
     C.ring_allreduce = E.ring_allreduce = ring_allreduce
     E.InProcTransport = transport
+    E.barrier = barrier
 
     def undo():
         C.ring_allreduce = E.ring_allreduce = orig_ring
         E.InProcTransport = orig_transport
+        E.barrier = orig_barrier
         for tr in live:
             tr.close()
 

@@ -30,7 +30,7 @@ EXPORTS = (
     "gp_gather_sum", "gp_broadcast", "gp_gather_sum_emulated", "gp_broadcast_emulated",
     "gp_comm_poll_error", "gp_get_stats",
     "gp_reset_stats", "gp_encode", "gp_decode", "gp_roundtrip", "gp_consume_update", "gp_consume_update_dev",
-    "gp_calib_p2p_copy", "gp_calib_p2p_copy_ex", "gp_calib_pingpong", "gp_calib_hop", "gp_comm_barrier", "gp_last_error_string", "gp_version",
+    "gp_calib_p2p_copy", "gp_calib_p2p_copy_ex", "gp_calib_pingpong", "gp_calib_hop", "gp_comm_barrier", "gp_comm_wire_bytes", "gp_last_error_string", "gp_version",
 )
 
 
@@ -80,8 +80,9 @@ _SIGS = {
     "gp_calib_p2p_copy": (_i, [_vp, _vp, _u64, _i, _i, _vp]),
     "gp_calib_p2p_copy_ex": (_i, [_vp, _vp, _u64, _i, _i, _u64, _vp, _vp, _vp]),
     "gp_calib_pingpong": (_i, [_vp, _vp, _i, _i, _u64, _vp, _vp]),
-    "gp_calib_hop": (_i, [_i, _vp, _vp, _vp, _vp, _u64, _vp, _vp]),
+    "gp_calib_hop": (_i, [_i, _vp, _vp, _vp, _vp, _u64, _i, _vp, _vp]),
     "gp_comm_barrier": (_i, [_vp, _i, _vp, _vp]),
+    "gp_comm_wire_bytes": (_i, [_vp, _i, _i, ctypes.POINTER(ctypes.c_uint64)]),
     "gp_last_error_string": (ctypes.c_char_p, []),
     "gp_version": (_i, []),
 }

@@ -203,9 +203,18 @@ __device__ __forceinline__ FV<E> load_fv(const float* x, uint64_t g0, uint64_t l
 // L2 eviction-priority policies (createpolicy) for streams read twice: the
 // first read marks lines evict_last so the second read finds them in the
 // 126 MB L2; the second read marks them evict_first (their last use).
+#ifndef PIPESGD_L2_KEEP
+#define PIPESGD_L2_KEEP 1  // 1: evict_last, 2: evict_normal, 0: evict_first (A/B knob)
+#endif
 __device__ __forceinline__ uint64_t l2_evict_last() {
   uint64_t p;
+#if PIPESGD_L2_KEEP == 1
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#elif PIPESGD_L2_KEEP == 2
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
   return p;
 }
 __device__ __forceinline__ uint64_t l2_evict_first() {

@@ -86,13 +86,12 @@ __global__ void __launch_bounds__(kT) absmax_kernel(const float* __restrict__ x,
                                                     gp_codec_status* st) {
   __shared__ uint32_t red[kT / 32];
   uint32_t m = 0;
-  int bad = 0;
-  GROUP_LOOP(4) {
-    const FV<4> v = load_fv<4>(x, g0, 0, n);
-    m = max(m, absmax_bits(v));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) bad |= nonfinite(v.v[i]);
-  }
+  // 4 float4 loads in flight per thread per iteration (a load-only pass:
+  // bytes in flight, not instructions, bound it); NaN bits compare above
+  // +inf as unsigned, so max|x| >= 0x7F800000 flags every non-finite value
+  stream_groups<16>(n, [&](uint64_t g0) { return load_fv<16>(x, g0, 0, n); },
+                    [&](uint64_t, const FV<16>& v) { m = max(m, absmax_bits(v)); });
+  int bad = m >= 0x7F800000u;
   m = cta_max_u32<kT>(m, red);
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
@@ -311,7 +310,7 @@ int gp_consume_update(float* w, int codec, const void* slot, const float* scale,
 }
 
 int gp_calib_hop(int codec, const float* x, const void* in, const float* in_scale, void* out, uint64_t n,
-                 gp_codec_status* st, void* stream) {
+                 int grid, gp_codec_status* st, void* stream) {
   if (codec < 0 || codec > 2) return cfail(GP_ERR_ARG, "unknown codec");
   if (!st) return cfail(GP_ERR_ARG, "null status");
   if (n && (!x || !in || !out)) return cfail(GP_ERR_ARG, "null buffer");
@@ -321,7 +320,7 @@ int gp_calib_hop(int codec, const float* x, const void* in, const float* in_scal
   cudaError_t e = cudaMemsetAsync(st, 0, sizeof(*st), s);
   if (e != cudaSuccess) return cfail(GP_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   if (n == 0) return GP_OK;
-  const uint32_t g = grid_for(n);
+  const uint32_t g = grid > 0 ? (uint32_t)grid : grid_for(n);
   auto* pi = static_cast<const uint8_t*>(in);
   auto* po = static_cast<uint8_t*>(out);
   if (codec == kQuant8) {

@@ -651,6 +651,18 @@ int gp_comm_barrier(gp_comm* c, int rounds, void* ns_out, void* stream) {
   return e == cudaSuccess ? GP_OK : cuda_fail(e, "barrier kernel launch");
 }
 
+int gp_comm_wire_bytes(gp_comm* c, int rank, int reset, uint64_t* out) {
+  if (!c || !out) return fail(GP_ERR_ARG, "null argument");
+  const int i = c->nlocal == 1 ? 0 : rank;
+  if (i < 0 || i >= c->nlocal) return fail(GP_ERR_ARG, "rank outside communicator");
+  DeviceGuard g(c->device);
+  uint8_t* p = c->inbox[i] + c->L.off_ctl + offsetof(Ctl, wire_bytes);
+  cudaError_t e = cudaMemcpy(out, p, sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(wire bytes)");
+  if (reset && (e = cudaMemset(p, 0, sizeof(uint64_t))) != cudaSuccess) return cuda_fail(e, "reset wire bytes");
+  return GP_OK;
+}
+
 int gp_comm_poll_error(gp_comm* c, gp_error* out) {
   if (!c || !out) return fail(GP_ERR_ARG, "null argument");
   DeviceGuard g(c->device);

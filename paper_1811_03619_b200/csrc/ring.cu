@@ -413,7 +413,12 @@ __device__ __noinline__ bool ring_access_ok(const void* ptr, uint64_t bytes, boo
   bool ok = (!write && in(R.x, 4 * P.n)) || in(R.out, 4 * P.n) || in(R.slot, w * P.n);
   for (int q = 0; q < P.p && !ok; ++q) {
     const uint64_t base = reinterpret_cast<uint64_t>(R.peer[q]);
-    if (a >= base && a < base + P.L.total_bytes) ok = inbox_region_ok(P.L, a - base, b - base);
+    if (a >= base && a < base + P.L.total_bytes) {
+      ok = inbox_region_ok(P.L, a - base, b - base);
+      // the bytes a real run moves over NVLink: stores into another rank's inbox
+      if (ok && write && q != R.rank)
+        atomicAdd(&reinterpret_cast<Ctl*>(R.inbox + P.L.off_ctl)->wire_bytes, (unsigned long long)bytes);
+    }
   }
   if (!ok) bounds_violation(a);
   return ok;

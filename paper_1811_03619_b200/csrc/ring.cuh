@@ -66,6 +66,7 @@ struct Ctl {                   // rank-private control block (peers write abort 
   CtlBank bank[2];
   unsigned long long ack[kMaxRanks];  // star calls: == seq once rank q consumed this rank's data
   unsigned long long barflag[kMaxRanks];  // gp_comm_barrier: generation rank q reached (written by q)
+  unsigned long long wire_bytes;          // bounds-checked build: payload bytes this rank stored into peers
 };
 static_assert(sizeof(Ctl) <= 2048, "ctl block: the p = 1 codec status lives at +2048");
 

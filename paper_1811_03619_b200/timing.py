@@ -219,11 +219,13 @@ def calibrate_nvlink(devices=(0, 1), nbytes: int = 1 << 30, ctas: int = 148, ite
     return {"alpha_s": alpha, "beta_s_per_byte": beta, "push_gbs": 1 / beta / 1e9}
 
 
-def gamma_hop(codec, n: int, device, reps: int = 10) -> float:
+def gamma_hop(codec, n: int, device, reps: int = 10, ring_ctas: int = 0) -> float:
     """Eq. 5's gamma on this GPU: seconds per payload byte of one fused
     reduce-scatter hop out = C(x + D(in)) over an n-element block (the
     reference calibrate()'s reduce_hop, harness.py:561-568), inputs cold in L2
-    (a 256 MiB read between launches, subtracted)."""
+    (a 256 MiB read between launches, subtracted). The probe's own launch
+    cost (the same hop over 16 elements) is subtracted too: the ring runs the
+    hop inside its one kernel, so only the per-byte rate belongs in Eq. 5."""
     import torch
 
     from . import _lib
@@ -252,14 +254,59 @@ def gamma_hop(codec, n: int, device, reps: int = 10) -> float:
                     flush.sum()
                     if hop:
                         _lib.call("gp_calib_hop", int(codec), x.data_ptr(), pay.data_ptr(), st_in.scale_view.data_ptr(),
-                                  out.data_ptr(), n, st.ptr, s.cuda_stream)
+                                  out.data_ptr(), n, (ring_ctas + 1) // 2, st.ptr, s.cuda_stream)
                 b.record(s)
             b.synchronize()
             return a.elapsed_time(b) / 1e3
 
         series(True)
         t = max(0.0, (series(True) - series(False)) / reps)
+    if n > 16:
+        t = max(0.0, t - gamma_hop(codec, 16, device, reps, ring_ctas) * 16 * w)
     return t / max(1, n * w)
+
+
+def delta_decode(codec, n: int, device, reps: int = 10) -> float:
+    """Seconds per element to decode a block into fp32 (the allgather's
+    receive side, which Eq. 5 has no term for), cold L2, launch cost of a
+    16-element decode subtracted."""
+    import torch
+
+    from . import _lib
+    from .compression import CodecStatus, as_codec, encode_async
+
+    codec = as_codec(codec)
+    w = codec.bytes_per_elem
+    with torch.cuda.device(device):
+        s = torch.cuda.Stream(device)
+        x = torch.randn(max(n, 16), device=device)
+        pay = torch.empty(max(16, x.numel() * w), dtype=torch.uint8, device=device)
+        st = CodecStatus(torch.device(device))
+        out = torch.empty_like(x)
+        flush = torch.ones(64 << 20, dtype=torch.float32, device=device)
+        with torch.cuda.stream(s):
+            encode_async(x, codec, pay, st, s.cuda_stream)
+
+        def series(m: int, dec: bool) -> float:
+            s.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                flush.sum()
+                torch.cuda._sleep(2_000_000)
+                a.record(s)
+                for _ in range(reps):
+                    flush.sum()
+                    if dec:
+                        _lib.call("gp_decode", int(codec), pay.data_ptr(), st.scale_view.data_ptr(), m,
+                                  out.data_ptr(), s.cuda_stream)
+                b.record(s)
+            b.synchronize()
+            return a.elapsed_time(b) / 1e3
+
+        series(n, True)
+        base = series(n, False)
+        t = max(0.0, (series(n, True) - base) / reps - max(0.0, (series(16, True) - base) / reps))
+    return t / max(1, n)
 
 
 def barrier_time(endpoint, rounds: int = 200) -> float:
@@ -285,10 +332,16 @@ def barrier_time(endpoint, rounds: int = 200) -> float:
 
 
 def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: float, gamma: float, sync: float,
-                 flag_threshold: float = 0.25) -> dict:
+                 delta: float = 0.0, flag_threshold: float = 0.25) -> dict:
     """One prediction-vs-measurement row for a ring call (compare_prediction,
     harness.py:687-720, applied to Eq. 5 itself): n is the element count,
-    model bytes are the codec's payload (harness.py:562)."""
+    model bytes are the codec's payload (harness.py:562).
+
+    `eq5_ext` (an extension, not the paper's): Eq. 5 plus the two passes of
+    this ring that the model leaves out -- the step-0 encode of the own block
+    before the first hop, (1/p) n_b gamma (quant8: with its max pass), and
+    the allgather's decode of the p-1 received blocks into the fp32 output,
+    (p-1)/p n delta (delta = decode time per element)."""
     from .compression import as_codec
 
     nb = float(n * as_codec(codec).bytes_per_elem)
@@ -296,8 +349,15 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
                            model_bytes=nb)
     lat, bw, red, syn = _ring_terms(params, 1)
     pred = ring_comm_time(params)
+    step0 = nb / p * gamma if p > 1 else 0.0
+    ag = (p - 1) / p * n * delta
+    ext = pred + step0 + ag
     rel = (measured_s - pred) / pred if pred > 0 else float("inf")
+    rel_ext = (measured_s - ext) / ext if ext > 0 else float("inf")
     return {"n": n, "codec": as_codec(codec).name.lower(), "measured_ms": measured_s * 1e3, "eq5_ms": pred * 1e3,
-            "terms_us": {"latency": lat * 1e6, "bandwidth": bw * 1e6, "reduction": red * 1e6, "sync": syn * 1e6},
+            "terms_us": {"latency": lat * 1e6, "bandwidth": bw * 1e6, "reduction": red * 1e6, "sync": syn * 1e6,
+                         "ext_step0_encode": step0 * 1e6, "ext_allgather_decode": ag * 1e6},
             "eq5_over_measured": pred / measured_s if measured_s > 0 else None, "rel_error": rel,
-            "flagged": abs(rel) > flag_threshold}
+            "flagged": abs(rel) > flag_threshold,
+            "eq5_ext_ms": ext * 1e3, "eq5_ext_over_measured": ext / measured_s if measured_s > 0 else None,
+            "ext_flagged": abs(rel_ext) > flag_threshold}

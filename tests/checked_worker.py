@@ -27,10 +27,24 @@ from paper_1811_03619_b200.collective import allreduce_into, endpoint_wait  # no
 assert os.path.basename(_lib.LIB_PATH) == "libpipesgd_checked.so", _lib.LIB_PATH
 
 
+def wire_bytes(ep, reset=True):
+    import ctypes
+    v = ctypes.c_uint64()
+    _lib.call("gp_comm_wire_bytes", ep._comm, ep.rank, int(reset), ctypes.byref(v))
+    return int(v.value)
+
+
+WIRE = []  # (p, n, codec, protocol, kernel-counted bytes, reference payload bytes), summed over ranks
+
+
 def run_case(tr, p, n, codec, fused, seed):
+    import ctypes
     g = np.random.default_rng(seed)
     ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
     w = P.Codec(codec).bytes_per_elem
+    for r in range(p):
+        wire_bytes(tr.endpoint(r))
+        tr.endpoint(r).reset_stats()
 
     def op(r, ep):
         dev = ep.device
@@ -50,6 +64,16 @@ def run_case(tr, p, n, codec, fused, seed):
             return out.cpu().numpy()
 
     res = run_ranks(tr, op)
+    got = sum(wire_bytes(tr.endpoint(r)) for r in range(p))
+    want = sum(tr.endpoint(r).stats.payload_bytes for r in range(p))
+    o = (ctypes.c_int64 * 5)()
+    _lib.call("gp_ring_plan", n, p, tr.endpoint(0).info()["ctas"], codec, 1 if fused else 0, n, o)
+    ll = bool(o[2])
+    WIRE.append((p, n, codec, "LL" if ll else "flag", got, want))
+    if not ll:  # every payload byte the reference hands its transport, stored exactly once into a peer
+        assert got == want, (p, n, codec, fused, got, want)
+    else:  # LL: every 4 payload bytes travel in an 8-byte word, plus header lines and group padding
+        assert 2 * want <= got <= 2 * want + 256 * p * p, (p, n, codec, got, want)  # edge groups, header lines
     if fused:
         summed = OR.ring_allreduce_all([OC.roundtrip(v, codec) for v in ins], codec).outputs[0]
         s_want, pl_want = OC.encode(summed, codec)
@@ -90,6 +114,8 @@ def main():
                     run_case(tr, p, n, codec, fused, 7 * n + codec)
         tr.close()
         print(f"per-rank p={p} ok", flush=True)
+    import json
+    print("WIRE " + json.dumps(WIRE))
     print("CHECKED OK")
 
 

@@ -167,8 +167,11 @@ def main():
                 rec["clocks"] = clk.summary()
             if sym is not None and rank == 0:
                 from paper_1811_03619_b200 import timing as T
-                gam = T.gamma_hop(codec, max(1, n // p), torch.device("cuda", local))
-                rec["eq5"] = T.compare_ring(t, p, codec, n, sym["alpha_s"], sym["beta_s_per_byte"], gam, sym["S_s"])
+                dv = torch.device("cuda", local)
+                gam = T.gamma_hop(codec, max(1, n // p), dv, ring_ctas=ep.info()["ctas"])
+                dlt = T.delta_decode(codec, max(1, n // p), dv)
+                rec["eq5"] = T.compare_ring(t, p, codec, n, sym["alpha_s"], sym["beta_s_per_byte"], gam, sym["S_s"],
+                                            dlt)
                 rec["eq5"]["gamma_gbs"] = 1 / gam / 1e9 if gam > 0 else None
             if args.cpu_ref_max and n <= args.cpu_ref_max:
                 dist.barrier()
