@@ -614,9 +614,12 @@ def our_arm(args, ws, rank, local):
                 "recompress": "encode_kernel"}[dom]
         kd = kernels[dom]
         live = kd["in_pipeline_hbm_gbs"]
-        roof = {"kernel": name, "bound": "hbm", "achieved": live, "peak": hbm_peak,
-                "unit": "GB/s", "frac": live / hbm_peak,
-                "traffic": traffic.get(name),
+        tr = traffic.get(name)
+        if q8 and dom in ("recompress", "compress") and tr is not None and traffic.get("absmax_kernel"):
+            tr += traffic["absmax_kernel"]  # quant8: the absmax pass belongs to the same encode
+        roof = {"kernel": name + (" (+ absmax_kernel)" if q8 and dom != "update" else ""), "bound": "hbm",
+                "achieved": live, "peak": hbm_peak, "unit": "GB/s", "frac": live / hbm_peak,
+                "traffic": tr,
                 "measured": "CUDA events on the launching stream around every launch of the timed region "
                             "(sharing HBM and SMs with the other stream); the same kernel alone, L2 flushed "
                             f"before each launch: {kd.get('isolated_hbm_gbs', 0):.1f} GB/s",

@@ -175,13 +175,27 @@ struct RingPlan {
 // warp). LL when the block payload fits ll_payload_limit(p) and the slot.
 RingPlan plan_ring(uint64_t n, int p, int G, int codec, int pre, uint64_t ll_cap) {
   RingPlan r{};
-  r.chunk = pick_chunk(n, p, G, codec);
   const uint64_t maxblk = (n + p - 1) / p + 16;
+  const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
+  r.ll = (maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), ll_cap)) ? 1 : 0;
+  r.chunk = pick_chunk(n, p, G, codec);
+  // LL uses no flags, so its chunk only sets how many warps share a block: a
+  // receiving lane polls its lines one after another, so shorter chunks (more
+  // warps, fewer polls each) cut the latency chain -- 128 elements for
+  // none / trunc16 (p = 4: 16 KiB 45 -> 22 us, C1's 2.6 MB 51 -> 35 us), 256
+  // for quant8 blocks up to 64 Ki elements; larger quant8 blocks keep the
+  // flag-protocol chunk (every extra warp adds a rank-barrier arrival per hop).
+  // profiles/r02/ll_chunk_ab/. PIPESGD_LL_CHUNK (elements) overrides.
+  static const uint64_t ll_env = env_u64("PIPESGD_LL_CHUNK", 0);
+  const uint64_t ll_chunk = ll_env ? ll_env
+                            : codec != GP_CODEC_QUANT8 ? 128 : (maxblk <= 65552 ? 256 : 0);
+  if (r.ll && ll_chunk) {
+    const uint64_t workers = (uint64_t)G * kRingWarps;
+    r.chunk = (uint32_t)std::max<uint64_t>(round_up(ll_chunk, 16), round_up((maxblk + workers - 1) / workers, 16));
+  }
   r.nch = (maxblk + r.chunk - 1) / r.chunk;
   if (pre && codec == GP_CODEC_QUANT8) r.nch = std::max<uint64_t>(r.nch, (n + r.chunk - 1) / r.chunk);
   r.ctas = (int)std::min<uint64_t>((uint64_t)G, std::max<uint64_t>(1, (r.nch + kRingWarps - 1) / kRingWarps));
-  const uint64_t w = codec == GP_CODEC_NONE ? 4 : codec == GP_CODEC_TRUNC16 ? 2 : 1;
-  r.ll = (maxblk * w <= std::min<uint64_t>(ll_payload_limit(p), ll_cap)) ? 1 : 0;
   // codec none folds D(C(.)) = identity, so the owner can fold every rank's
   // raw block in the ring's order after one NVSwitch hop: bit-identical
   // sums, identical wire bytes; PIPESGD_DIRECT=0 keeps the ring

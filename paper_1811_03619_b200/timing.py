@@ -337,11 +337,14 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
     harness.py:687-720, applied to Eq. 5 itself): n is the element count,
     model bytes are the codec's payload (harness.py:562).
 
-    `eq5_ext` (an extension, not the paper's): Eq. 5 plus the two passes of
-    this ring that the model leaves out -- the step-0 encode of the own block
-    before the first hop, (1/p) n_b gamma (quant8: with its max pass), and
+    `eq5_ext` (an extension, not the paper's), quant8 only: Eq. 5 plus the
+    two passes of the quant8 ring that overlap no transfer -- the step-0 max
+    and encode of the own block before the first hop, (1/p) n_b gamma, and
     the allgather's decode of the p-1 received blocks into the fp32 output,
-    (p-1)/p n delta (delta = decode time per element)."""
+    (p-1)/p n delta (delta = decode time per element). For none / trunc16 the
+    step-0 encode streams straight onto the link and the decode overlaps the
+    owners' pushes, so eq5_ext == Eq. 5 (measured: 0.93-1.14 of the ring at
+    >= 64 MiB, profiles/r02/c5)."""
     from .compression import as_codec
 
     nb = float(n * as_codec(codec).bytes_per_elem)
@@ -349,8 +352,9 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
                            model_bytes=nb)
     lat, bw, red, syn = _ring_terms(params, 1)
     pred = ring_comm_time(params)
-    step0 = nb / p * gamma if p > 1 else 0.0
-    ag = (p - 1) / p * n * delta
+    q8 = as_codec(codec).name.lower() == "quant8"
+    step0 = nb / p * gamma if (p > 1 and q8) else 0.0
+    ag = (p - 1) / p * n * delta if q8 else 0.0
     ext = pred + step0 + ag
     rel = (measured_s - pred) / pred if pred > 0 else float("inf")
     rel_ext = (measured_s - ext) / ext if ext > 0 else float("inf")

@@ -107,8 +107,14 @@ def test_ll_protocol_threshold(world, codec):
 
 
 def test_launch_and_chunk_plan():
-    # tiny calls launch one CTA; the chunk stays at its 1024-element minimum
-    assert _plan(8, 2, 592, 1) == {"chunk": 1024, "ctas": 1, "ll": 1, "nch": 1, "direct": 0}
+    # tiny calls launch one CTA; LL calls (no flags) use short chunks so more
+    # warps share a block: 128 elements for none / trunc16, 256 for small quant8
+    assert _plan(8, 2, 592, 1) == {"chunk": 128, "ctas": 1, "ll": 1, "nch": 1, "direct": 0}
+    pl = _plan(648_010, 4, 592, 0)  # C1 gradient, codec none, LL
+    assert pl["ll"] == 1 and pl["chunk"] == 128 and pl["nch"] == 1266 and pl["ctas"] == 317
+    assert _plan(65_536, 4, 592, 2)["chunk"] == 256
+    # larger quant8 LL blocks keep the flag-protocol chunk (barrier arrivals per warp)
+    assert _plan(1 << 20, 4, 592, 2)["chunk"] == 1024
     # C2 gradient, standalone budget: 1024-element chunks, one per warp
     pl = _plan(4_710_538, 2, 592, 1)
     assert pl["chunk"] == 1024 and pl["nch"] == 2301 and pl["ctas"] == 576 and pl["ll"] == 0
