@@ -53,8 +53,9 @@ def parse():
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--global-batch", type=int, default=None,
                     help="default: the paper's global batch for the config (100 MNIST, 512 CIFAR, 256 ImageNet)")
-    ap.add_argument("--ctas", type=int, default=256,
-                    help="128-thread CTAs the ring kernel may occupy per GPU beside the compute stream")
+    ap.add_argument("--ctas", type=int, default=0,
+                    help="128-thread CTAs the ring kernel may occupy per GPU (0: engine.default_comm_ctas -- "
+                         "64 for Pipe-SGD on gradients <= 32 MB, else 256)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
                     help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync, fused)")
@@ -375,6 +376,7 @@ def workload_config(args, n, N):
             "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
             "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
             "cuda_graphs": bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused),
+            "ring_ctas": args.ctas or None,
             "model_math": "fp32 (TF32 disabled for cuDNN convolutions and cuBLAS matmuls)",
             "l2": "not flushed: each step streams the model's activations for the per-GPU batch plus the "
                   "gradient, weights and slots through HBM"}
@@ -399,6 +401,9 @@ def our_arm(args, ws, rank, local):
     fm = FlatModel(mod, dev)
     n = fm.num_params
     cap = max(n, 1 << 26) if N > 1 else (n if args.mode == "ps_sync" else 1 << 10)
+    if not args.ctas:
+        from paper_1811_03619_b200.engine import default_comm_ctas
+        args.ctas = default_comm_ctas(args.mode, n)
     if N > 1:
         ep = ProcessGroupTransport.endpoint(local, max_elems=cap, ctas=args.ctas, timeout_s=60.0)
     else:

@@ -34,8 +34,12 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 constexpr uint64_t kLLHopBytes = PIPESGD_LL_HOP_BYTES;
 constexpr uint64_t kLLRegionBytes = PIPESGD_LL_REGION_BYTES;  // largest LL block payload (fixed: layouts agree)
 
+// p = 2 takes LL up to 1 MiB blocks (with the short LL chunks, trunc16 at
+// C1's size 27 -> 16 us, quant8 at 4 MiB 40 -> 32 us); from p = 3 on, LL
+// above 512 KiB x (p - 1) lost to the flag protocol (none at 8 MiB, p = 4:
+// 71 -> 79 us). profiles/r02/ll_threshold_ab/.
 __host__ __device__ inline uint64_t ll_payload_limit(int p) {
-  const uint64_t v = kLLHopBytes * (uint64_t)(p > 1 ? p - 1 : 1);
+  const uint64_t v = p == 2 ? 2 * kLLHopBytes : kLLHopBytes * (uint64_t)(p > 1 ? p - 1 : 1);
   return v < kLLRegionBytes ? v : kLLRegionBytes;
 }
 

@@ -709,12 +709,24 @@ class RankEngine:
 
 # ----------------------------------------------------------------- clusters
 
-# CTAs (128 threads each, 1024 warps in total) the ring kernel may occupy
-# while the compute stream runs the next iteration; they share SMs with the
-# forward/backward kernels. Iterations/s do not depend on it between 32 and
-# 256 CTAs (the ring stays hidden: profiles/r01_ring_latency/comm_ctas_ab.log);
-# 256 gives the shortest ring inside the step (C2, N=2: 64 us vs 76 us at 128).
+# CTAs (128 threads each) the ring kernel may occupy. D-Sync runs the ring
+# between computes: the full budget gives the shortest ring. Pipe-SGD runs it
+# beside the next iteration's forward/backward, and the ring's resident CTAs
+# (most of them waiting on flags) keep SMs from the compute kernels: for a
+# small gradient the budget is cut to 64 CTAs (C1 MLP, N = 4: 6067 -> 7602
+# iterations/s; compute 143 -> 110 us per step), while a large one keeps 256
+# so its longer ring stays hidden (C3 AlexNet: 191.0 at 256 vs 185.4 at 64;
+# C2: flat) -- profiles/r02/engine_ctas/.
 COMM_CTAS = 256
+PIPE_SMALL_GRADIENT_CTAS = 64
+SMALL_GRADIENT_BYTES = 32 << 20
+
+
+def default_comm_ctas(mode: str, num_params: int) -> int:
+    """The ring's CTA budget for a training run (see COMM_CTAS)."""
+    if mode == MODE_PIPE_SGD and 4 * num_params <= SMALL_GRADIENT_BYTES:
+        return PIPE_SMALL_GRADIENT_CTAS
+    return COMM_CTAS
 
 
 def _make_transport(workers: int, timeout_s: float, max_elems: int, ctas: int = COMM_CTAS):
@@ -741,7 +753,7 @@ class DeviceDataset:
 def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_s: float = 0.0,
                        byte_time_s: float = 0.0, batch_provider=None, timeout_s: float = 30.0,
                        transport=None, grad_fn=None, trace: bool = True, fused: bool = True,
-                       comm_ctas: int = COMM_CTAS) -> list[WorkerResult]:
+                       comm_ctas: int | None = None) -> list[WorkerResult]:
     """Run a full training job with all ranks as threads of this process
     (engine.py:563-618), one GPU per rank (GpuTransport) or all ranks on one
     GPU (EmulatedTransport) when there are fewer GPUs than workers.
@@ -757,6 +769,8 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
         model = ModelSpec(model.kind, tuple(model.layer_dims))
     n = model.num_params
     own_transport = transport is None
+    if comm_ctas is None:
+        comm_ctas = default_comm_ctas(config.mode, n)
     tr = transport or _make_transport(workers, timeout_s, max(n, 1), comm_ctas)
     shards = [np.arange(r % workers, dataset.features.shape[0], workers) for r in range(workers)]
     if batch_provider is None and grad_fn is None:
@@ -820,7 +834,7 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
 
 
 def run_process_worker(config: RunConfig, dataset, model, timeout_s: float = 30.0, batch_provider=None,
-                       grad_fn=None, trace: bool = True, fused: bool = True, comm_ctas: int = COMM_CTAS,
+                       grad_fn=None, trace: bool = True, fused: bool = True, comm_ctas: int | None = None,
                        group=None) -> WorkerResult:
     """One rank of a multi-process run (one process per GPU under torchrun):
     the analogue of the reference's run_tcp_worker (engine.py:621-646).
@@ -841,7 +855,8 @@ def run_process_worker(config: RunConfig, dataset, model, timeout_s: float = 30.
     if not isinstance(model, ModelSpec):
         model = ModelSpec(model.kind, tuple(model.layer_dims))
     ep = ProcessGroupTransport.endpoint(local, group=group, timeout_s=timeout_s,
-                                        max_elems=max(model.num_params, 1), ctas=comm_ctas)
+                                        max_elems=max(model.num_params, 1),
+                                        ctas=comm_ctas or default_comm_ctas(config.mode, model.num_params))
     dev = ep.device
     shard = np.arange(rank % workers, dataset.features.shape[0], workers)
     if batch_provider is None and grad_fn is None and config.batch_size > len(shard):

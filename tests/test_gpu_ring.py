@@ -255,14 +255,14 @@ def test_p2p_iteration_tag_mismatch_is_a_header_error(P, n):
 
 @multigpu
 def test_p2p_ll_threshold_and_protocol_switching(P):
-    """Sizes either side of the LL threshold (at p = 2, none/trunc16 blocks
-    whose payload incl. 16 elements of slack is <= 512 KiB use the
-    sequence-tagged LL slots, larger ones the flag protocol), called
-    alternately on one communicator: every result equals the reference's, so
-    neither protocol ever reads the other's stale bytes."""
+    """Sizes either side of the LL threshold (at p = 2, blocks whose payload
+    incl. 16 elements of slack is <= 1 MiB use the sequence-tagged LL slots,
+    larger ones the flag protocol), called alternately on one communicator:
+    every result equals the reference's, so neither protocol ever reads the
+    other's stale bytes."""
     p = 2
-    t = 2 * ((512 << 10) // 4 - 16)  # fp32 threshold; trunc16's is twice that
-    sizes = [8, t - 1, t, t + 1, t + 33, 2 * t, 2 * t + 2, 1_000_003, 8, t, 5]
+    t = 2 * ((1 << 20) // 4 - 16)  # fp32 threshold; trunc16's is twice that, quant8's 4x
+    sizes = [8, t - 1, t, t + 1, t + 33, 2 * t, 2 * t + 2, 4 * t + 2, 1_000_003, 8, t, 5]
     tr = real_transport(P, p, timeout_s=30.0, max_elems=max(sizes))
     try:
         for k, n in enumerate(sizes):
