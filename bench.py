@@ -53,9 +53,9 @@ def parse():
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--global-batch", type=int, default=None,
                     help="default: the paper's global batch for the config (100 MNIST, 512 CIFAR, 256 ImageNet)")
-    ap.add_argument("--ctas", type=int, default=0,
-                    help="128-thread CTAs the ring kernel may occupy per GPU (0: engine.default_comm_ctas -- "
-                         "64 for Pipe-SGD on gradients <= 32 MB, else 256)")
+    ap.add_argument("--ctas", type=int, default=-1,
+                    help="128-thread CTAs the ring kernel may occupy per GPU (-1: engine.default_comm_ctas -- "
+                         "64 for Pipe-SGD on gradients <= 32 MB, else every SM; 0: every SM)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
                     help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync, fused)")
@@ -376,7 +376,7 @@ def workload_config(args, n, N):
             "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
             "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
             "cuda_graphs": bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused),
-            "ring_ctas": args.ctas or None,
+            "ring_ctas": args.ctas if args.ctas > 0 else None,
             "model_math": "fp32 (TF32 disabled for cuDNN convolutions and cuBLAS matmuls)",
             "l2": "not flushed: each step streams the model's activations for the per-GPU batch plus the "
                   "gradient, weights and slots through HBM"}
@@ -401,7 +401,7 @@ def our_arm(args, ws, rank, local):
     fm = FlatModel(mod, dev)
     n = fm.num_params
     cap = max(n, 1 << 26) if N > 1 else (n if args.mode == "ps_sync" else 1 << 10)
-    if not args.ctas:
+    if args.ctas < 0:
         from paper_1811_03619_b200.engine import default_comm_ctas
         args.ctas = default_comm_ctas(args.mode, n)
     if N > 1:
@@ -409,6 +409,7 @@ def our_arm(args, ws, rank, local):
     else:
         tr = GpuTransport(1, max_elems=cap, ctas=args.ctas)
         ep = tr.endpoint(0)
+    args.ctas = ep.info()["ctas"]  # the budget the ring actually runs with (reported in config)
     B = args.global_batch // N
     total_steps = 2 * (args.warmup + args.steps) + 8
     cfg = RunConfig(mode=args.mode, iterations=total_steps, learning_rate=0.01, codec=args.codec,

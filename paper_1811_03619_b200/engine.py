@@ -709,15 +709,16 @@ class RankEngine:
 
 # ----------------------------------------------------------------- clusters
 
-# CTAs (128 threads each) the ring kernel may occupy. D-Sync runs the ring
-# between computes: the full budget gives the shortest ring. Pipe-SGD runs it
-# beside the next iteration's forward/backward, and the ring's resident CTAs
-# (most of them waiting on flags) keep SMs from the compute kernels: for a
-# small gradient the budget is cut to 64 CTAs (C1 MLP, N = 4: 6067 -> 7602
-# iterations/s; compute 143 -> 110 us per step), while a large one keeps 256
-# so its longer ring stays hidden (C3 AlexNet: 191.0 at 256 vs 185.4 at 64;
-# C2: flat) -- profiles/r02/engine_ctas/.
-COMM_CTAS = 256
+# CTAs (128 threads each) the ring kernel may occupy; 0 = the communicator's
+# default, every SM (4 CTAs per SM). D-Sync runs the ring between computes:
+# the full budget gives the shortest ring. Pipe-SGD runs it beside the next
+# iteration's forward/backward, and the ring's resident CTAs (most of them
+# waiting on flags) keep SMs from the compute kernels: for a small gradient
+# the budget is cut to 64 CTAs (C1 MLP, N = 4: 6067 -> 7602 iterations/s at
+# 256 -> 64; compute 143 -> 110 us per step), while a large one is best
+# finished fast (C3 AlexNet: 185.4 / 191.7 / 195.1 / 197.4 iterations/s at
+# 64 / 256 / 384 / 592 CTAs; C2, C4: flat) -- profiles/r02/engine_ctas/.
+COMM_CTAS = 0
 PIPE_SMALL_GRADIENT_CTAS = 64
 SMALL_GRADIENT_BYTES = 32 << 20
 
