@@ -444,10 +444,17 @@ def our_arm(args, ws, rank, local):
 
     copy_events = []
 
+    copy_after_ring = os.environ.get("BENCH_COPY_AFTER_RING", "1") == "1"
+
     def prefetch(tt):
-        """H2D copy of step tt's batch into its buffer, once the step that read it last is done."""
+        """H2D copy of step tt's batch into its buffer, once the step that read it last is done.
+        Pipe-SGD under graphs: also after the ring of step tt-2 -- it overlaps the start of step
+        tt-1's compute, and a PCIe copy landing beside both slowed that compute (C3, N=4: compute
+        4.90 -> 5.12 ms per step); the copy still has the rest of step tt-1 (~4 ms) to finish."""
         b = tt % nb
         copy_stream.wait_event(bufs["free"][b])
+        if copy_after_ring and pipe and "graphs" in bufs and tt - 2 in eng.graph_ready_tag.values():
+            copy_stream.wait_event(eng.ev_agg[(tt - 2) % eng.K])
         c0 = torch.cuda.Event(enable_timing=True)
         c0.record(copy_stream)
         with torch.cuda.stream(copy_stream):

@@ -81,8 +81,12 @@ __device__ __forceinline__ Q8 q8_make(float s) {
 // +-inf in the reference -> +-127, and 0/0 casts to 0. x == 0 (either sign)
 // always yields 0. Inputs are the block's own values, so y <= 127 * (1 +
 // 2^-15); the clamp to 255 only keeps a NaN (already latched) harmless.
+// GENERAL = false: the common block (scale not tiny, not zero), where the
+// 2^64 lift and the zero-scale / zero-value selects are identities (a = 0
+// already gives y = 0 -> code 0); the caller branches once per group.
+template <bool GENERAL = true>
 __device__ __forceinline__ int q8_encode(float x, const Q8& q) {
-  const float a = __fmul_rn(fabsf(x), q.pre);
+  const float a = GENERAL ? __fmul_rn(fabsf(x), q.pre) : fabsf(x);
   const float y = fminf(__fmul_rn(a, q.inv), 255.f);
   const float t = __fadd_rn(y, 8388608.f);             // 2^23 + RN(y), exact integer in the mantissa
   const float k = fminf(__fsub_rn(t, 8388608.f), 127.f);
@@ -90,8 +94,10 @@ __device__ __forceinline__ int q8_encode(float x, const Q8& q) {
   const float r_lo = __fmaf_rn(__fsub_rn(k, 0.5f), q.ss, -a);  // > 0 : k too large
   const float r_hi = __fmaf_rn(__fadd_rn(k, 0.5f), q.ss, -a);  // <= 0: k too small
   c += ((c < 127) & (r_hi <= 0.f)) - ((c >= 1) & (r_lo > 0.f));
-  c = q.zero ? 127 : c;
-  c = (a == 0.f) ? 0 : c;
+  if constexpr (GENERAL) {
+    c = q.zero ? 127 : c;
+    c = (a == 0.f) ? 0 : c;
+  }
   return (x < 0.f) ? -c : c;
 }
 // code -> exact float without I2F: the byte c + 128 under the exponent of
@@ -119,8 +125,11 @@ __device__ __forceinline__ uint32_t wget(const uint4& p, int i) {
 }
 
 // CHECK = false where the caller has already established finiteness (the
-// quant8 ring: pass A's block max covers every value pass B encodes)
-template <int C, bool CHECK = true>
+// quant8 ring: pass A's block max covers every value pass B encodes).
+// FAST = true branches once per group to the common-block quant8 encoder
+// (q8_encode<false>); the ring keeps the single path (its 128-register
+// budget has no room for both).
+template <int C, bool CHECK = true, bool FAST = false>
 __device__ __forceinline__ uint4 encode_v(const FV<CodecT<C>::E>& v, const Q8& q, int& bad) {
   constexpr int E = CodecT<C>::E;
   uint32_t w[4];
@@ -135,14 +144,16 @@ __device__ __forceinline__ uint4 encode_v(const FV<CodecT<C>::E>& v, const Q8& q
 #pragma unroll
     for (int i = 0; i < 4; ++i) w[i] = t16_encode(v.v[2 * i]) | (t16_encode(v.v[2 * i + 1]) << 16);
   } else {
+    auto pack = [&](auto enc) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t x;
-      const uint32_t c0 = (uint32_t)q8_encode(v.v[4 * i], q), c1 = (uint32_t)q8_encode(v.v[4 * i + 1], q);
-      const uint32_t c2 = (uint32_t)q8_encode(v.v[4 * i + 2], q), c3 = (uint32_t)q8_encode(v.v[4 * i + 3], q);
-      x = __byte_perm(__byte_perm(c0, c1, 0x0040u), __byte_perm(c2, c3, 0x0040u), 0x5410u);  // low bytes c0..c3
-      w[i] = x;
-    }
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t c0 = (uint32_t)enc(v.v[4 * i]), c1 = (uint32_t)enc(v.v[4 * i + 1]);
+        const uint32_t c2 = (uint32_t)enc(v.v[4 * i + 2]), c3 = (uint32_t)enc(v.v[4 * i + 3]);
+        w[i] = __byte_perm(__byte_perm(c0, c1, 0x0040u), __byte_perm(c2, c3, 0x0040u), 0x5410u);  // bytes c0..c3
+      }
+    };
+    if (FAST && q.pre == 1.f && !q.zero) pack([&](float x) { return q8_encode<false>(x, q); });
+    else pack([&](float x) { return q8_encode<true>(x, q); });
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
 }

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kT, PIPESGD_CU_MINB) encode_kernel(const float
   int bad = 0;
   stream_groups<E>(n, [&](uint64_t g0) { return load_fv<E>(x, g0, 0, n); },
                    [&](uint64_t g0, const FV<E>& v) {
-                     store_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0), encode_v<C>(v, q, bad));
+                     store_pay<C>(payload, g0, 0, (int)(min(n, g0 + E) - g0), encode_v<C, true, true>(v, q, bad));
                    });
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kT) roundtrip_kernel(const float* __restrict__
   int bad = 0;
   stream_groups<E>(n, [&](uint64_t g0) { return load_fv<E>(x, g0, 0, n); },
                    [&](uint64_t g0, const FV<E>& v) {
-                     store_fv<E>(out, g0, 0, n, decode_v<C>(encode_v<C>(v, q, bad), q.s));
+                     store_fv<E>(out, g0, 0, n, decode_v<C>(encode_v<C, true, true>(v, q, bad), q.s));
                    });
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kT) hop_encode_kernel(const float* __restrict_
   stream_groups<E>(n, [&](uint64_t g0) { return XI{load_fv<E>(x, g0, 0, n), load_pay<C>(in, g0, 0, (int)(min(n, g0 + E) - g0))}; },
                    [&](uint64_t g0, const XI& v) {
                      store_pay<C>(out, g0, 0, (int)(min(n, g0 + E) - g0),
-                                  encode_v<C>(add_v(v.x, decode_v<C>(v.in, s)), q, bad));
+                                  encode_v<C, true, true>(add_v(v.x, decode_v<C>(v.in, s)), q, bad));
                    });
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->nonfinite, 1);
 }
