@@ -138,8 +138,9 @@ multigpu = pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
 
 
 @multigpu
-def test_p2p_ring_matches_reference_golden(P, gold):
-    p = 4
+@pytest.mark.parametrize("p", [4, 8])
+def test_p2p_ring_matches_reference_golden(P, gold, p):
+    """Per-rank launches; p = 8 pairs ranks on 4 GPUs (or shares one)."""
     tr = real_transport(P, p, timeout_s=30.0, max_elems=1 << 14)
     try:
         check_against_golden(P, tr, gold, p)
