@@ -11,7 +11,10 @@ namespace gp {
 #endif
 constexpr int kRingThreads = PIPESGD_RING_THREADS;
 constexpr int kRingWarps = kRingThreads / 32;
-constexpr uint32_t kMinChunk = 1024;   // elements per warp chunk; flags are sized for this
+#ifndef PIPESGD_MIN_CHUNK
+#define PIPESGD_MIN_CHUNK 1024
+#endif
+constexpr uint32_t kMinChunk = PIPESGD_MIN_CHUNK;  // elements per warp chunk; flags are sized for this
 constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of fp32)
 
 // Per-rank inbox layout (identical on every rank of a communicator). Peers

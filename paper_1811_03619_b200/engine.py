@@ -241,6 +241,9 @@ class RankEngine:
             self.slot_nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
             self.losses = torch.zeros(config.iterations + 2, dtype=torch.float32, device=self.dev)
         self.ev_local = [torch.cuda.Event() for _ in range(K)]
+        # gradient buffer i already zero (cleared by the comm stream after the
+        # fused ring / encode read it): the next backward into it skips its zero_
+        self.grad_clean = [True] * K
         self.buffer = GradientBuffer(K)
         self.iter_done: dict[int, torch.cuda.Event] = {}
         self._pending = None
@@ -289,8 +292,9 @@ class RankEngine:
             self.losses[t].fill_(float(loss))
         else:
             x, y = self.batch_fn(self.rank, t)
-            loss = self.fm.loss_and_grad(x, y)
+            loss = self.fm.loss_and_grad(x, y, zero=not (self.fused and self.grad_clean[i]))
             self.losses[t].copy_(loss)
+        self.grad_clean[i] = False
         e1 = self._ev(self.cs) if self.tracing else None
         if not self.fused:
             roundtrip_async(self.fm.grads, self.cfg.codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
@@ -352,6 +356,9 @@ class RankEngine:
                 allreduce_into(g, self.summed, self.ep, codec, t, self.ms, precompress=True)
             else:
                 roundtrip_async(g, codec, self.local[i], self.local_status[i], self.ms.cuda_stream)
+        with torch.cuda.stream(self.ms):  # ready for the backward of t + K (ordered after `ready` below)
+            g.zero_()
+        self.grad_clean[i] = True
         ready = torch.cuda.Event(enable_timing=self.tracing)
         ready.record(self.ms)
         if self.tracing:
@@ -489,7 +496,7 @@ class RankEngine:
             gc = torch.cuda.CUDAGraph()
             with capture(gc, self.cs):
                 self.fm.use_grad_buffer(i)
-                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
+                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i], zero=False))
             gm = torch.cuda.CUDAGraph()
             with capture(gm, self.ms):
                 g = self.fm.grad_bufs[i]
@@ -498,6 +505,7 @@ class RankEngine:
                                    slot=slot.payload, slot_scale=slot.status.scale_view)
                 else:
                     encode_async(g, cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
+                g.zero_()  # clean for the backward of t + K
             self.g_compute.append(gc)
             self.g_comm.append(gm)
         self.graph_ready_tag = {}
@@ -513,7 +521,7 @@ class RankEngine:
             gc = torch.cuda.CUDAGraph()
             with capture(gc, self.cs):
                 self.fm.use_grad_buffer(i)
-                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
+                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i], zero=False))
             gm = torch.cuda.CUDAGraph()
             with capture(gm, self.cs):
                 g = self.fm.grad_bufs[i]
@@ -521,6 +529,7 @@ class RankEngine:
                     allreduce_into(g, self.summed, self.ep, codec, 0, self.cs, precompress=True)
                 else:
                     roundtrip_async(g, codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+                g.zero_()  # clean for the backward of t + K
             self.g_update.append(gu)
             self.g_compute.append(gc)
             self.g_comm.append(gm)

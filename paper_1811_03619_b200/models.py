@@ -216,9 +216,13 @@ class FlatModel:
     def zero_grad(self):
         self.grads.zero_()
 
-    def loss_and_grad(self, x, y):
-        """Mean softmax cross-entropy; gradient lands in self.grads."""
-        self.grads.zero_()
+    def loss_and_grad(self, x, y, zero: bool = True):
+        """Mean softmax cross-entropy; gradient lands in self.grads (autograd
+        accumulates into it: zero=False when the caller guarantees the buffer
+        is already zero -- the engine clears it on the comm stream right after
+        the ring has read it, off the compute stream's critical path)."""
+        if zero:
+            self.grads.zero_()
         logits = self.module(x)
         loss = F.cross_entropy(logits, y)
         loss.backward()
