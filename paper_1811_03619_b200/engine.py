@@ -356,14 +356,15 @@ class RankEngine:
                 allreduce_into(g, self.summed, self.ep, codec, t, self.ms, precompress=True)
             else:
                 roundtrip_async(g, codec, self.local[i], self.local_status[i], self.ms.cuda_stream)
-        with torch.cuda.stream(self.ms):  # ready for the backward of t + K (ordered after `ready` below)
+        e1 = self._ev(self.ms) if self.tracing else None
+        with torch.cuda.stream(self.ms):  # clean for the backward of t + K (ordered before `ready`)
             g.zero_()
         self.grad_clean[i] = True
         ready = torch.cuda.Event(enable_timing=self.tracing)
         ready.record(self.ms)
         if self.tracing:
-            self._rec(t, STAGE_ALLREDUCE, e0, ready)
-            self._rec(t, "ring" if self.world > 1 else "recompress", e0, ready)
+            self._rec(t, STAGE_ALLREDUCE, e0, e1)
+            self._rec(t, "ring" if self.world > 1 else "recompress", e0, e1)
         self.buffer.put(t, slot, ready)
         return slot
 
@@ -505,7 +506,6 @@ class RankEngine:
                                    slot=slot.payload, slot_scale=slot.status.scale_view)
                 else:
                     encode_async(g, cfg.codec, slot.payload, slot.status, self.ms.cuda_stream)
-                g.zero_()  # clean for the backward of t + K
             self.g_compute.append(gc)
             self.g_comm.append(gm)
         self.graph_ready_tag = {}
@@ -529,7 +529,6 @@ class RankEngine:
                     allreduce_into(g, self.summed, self.ep, codec, 0, self.cs, precompress=True)
                 else:
                     roundtrip_async(g, codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
-                g.zero_()  # clean for the backward of t + K
             self.g_update.append(gu)
             self.g_compute.append(gc)
             self.g_comm.append(gm)
@@ -557,8 +556,9 @@ class RankEngine:
         if self.world > 1:
             self.tag_dev.fill_(t)
         self.g_comm[i].replay()
+        e3 = self._ev(self.cs) if tr else None
+        self.fm.grad_bufs[i].zero_()  # clean for the backward of t + K
         if tr:
-            e3 = self._ev(self.cs)
             self._rec(t, STAGE_UPDATE, e0, e1, t - 1)
             self._rec(t, STAGE_BACKWARD, e1, e2)
             self._rec(t, STAGE_ALLREDUCE, e2, e3)
@@ -591,11 +591,13 @@ class RankEngine:
             if self.world > 1:
                 self.tag_dev.fill_(t)
             self.g_comm[i].replay()
+        e2 = self._ev(self.ms) if tr else None
+        with torch.cuda.stream(self.ms):  # clean for the backward of t + K (outside the timed ring)
+            self.fm.grad_bufs[i].zero_()
         self.ev_agg[i].record(self.ms)
         if tr:
             self._rec(t, STAGE_UPDATE, e0, eu, t - self.K)
             self._rec(t, STAGE_BACKWARD, eu, self._ev(self.cs))
-            e2 = self._ev(self.ms)
             self._rec(t, STAGE_ALLREDUCE, e1, e2)
             self._rec(t, "ring" if self.world > 1 else "recompress", e1, e2)
         self.graph_ready_tag[i] = t
