@@ -55,7 +55,7 @@ def parse():
                     help="default: the paper's global batch for the config (100 MNIST, 512 CIFAR, 256 ImageNet)")
     ap.add_argument("--ctas", type=int, default=-1,
                     help="128-thread CTAs the ring kernel may occupy per GPU (-1: engine.default_comm_ctas -- "
-                         "64 for Pipe-SGD on gradients <= 32 MB, else every SM; 0: every SM)")
+                         "Pipe-SGD 64 on gradients <= 32 MB else 256, D-Sync every SM; 0: every SM)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
                     help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync, fused)")

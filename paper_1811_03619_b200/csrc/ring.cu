@@ -63,6 +63,15 @@ __shared__ uint32_t s_bank;                 // ctl bank of this call (ring.cuh:C
 __shared__ unsigned long long s_calls;      // raw count of calls completed before this one
 __shared__ unsigned long long s_abort;      // the abort word at kernel entry
 __shared__ uint32_t s_iter;                 // iteration tag of this call (argument or device word)
+// quant8 rank barriers, CTA-aggregated: the CTA's warps meet in shared
+// memory, the last one to arrive makes the CTA's single global arrival and
+// polls the rank counter, the others wait on s_bar_open (one barrier index k
+// per rank barrier of the call, k < 16)
+constexpr int kMaxBarriers = 16;
+__shared__ unsigned s_bar_arrived[kMaxBarriers];
+__shared__ unsigned s_bar_max[kMaxBarriers];
+__shared__ float s_bar_vmax[kMaxBarriers];
+__shared__ int s_bar_open[kMaxBarriers];    // 0 waiting, 1 open, 2 failed
 #ifdef PIPESGD_CHECKED
 __shared__ const RingParams* s_P;           // launch parameters (bounds checks)
 #endif
@@ -257,41 +266,75 @@ __device__ __forceinline__ void warp_publish_all(const RingParams& P, const Rank
   }
 }
 
-// quant8: rank-wide barrier over all G x kWarps warps of one rank carrying the
-// block max. Returns false on abort/timeout.
+// quant8: rank-wide barrier over all G CTAs of one rank carrying the block
+// max. The CTA's warps meet in shared memory; the last warp of the CTA to
+// arrive publishes the CTA max and one arrival to the rank's control block
+// (4x fewer same-address atomics than per-warp arrivals, which serialised in
+// L2) and polls for the rank count; the other warps spin on shared memory.
+// Returns false on abort/timeout (a warp that left early never arrives: the
+// rest time out, as everywhere else in the kernel).
 __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl, ErrWord* err, int k,
                                  uint32_t mymax, float& vmax, int step) {
-  // every lane's pass-A stores (the partials in `out`) must be ordered
-  // before lane 0's arrival: __syncwarp orders them within the warp, and
-  // lane 0's fence below is cumulative over what it has observed
+  // every lane's earlier stores and the warp's global max-slot atomics are
+  // ordered before its arrival: __syncwarp orders the lanes, and the fences
+  // below are cumulative over what lane 0 has observed
   __syncwarp();
   const uint32_t m = warp_max_u32(mymax);
   int ok = 1;
   float v = 0.f;
   if (lane_id() == 0) {
-    atomicMax(&cb(ctl)->maxslot[k], ((unsigned long long)s_seq << 32) | m);
-    __threadfence();
-    atomicAdd(&cb(ctl)->bar, 1ull);
-    const unsigned long long target = (unsigned long long)(k + 1) * P.G * kWarps;
+    atomicMax(&s_bar_max[k], m);
+    __threadfence();  // this warp's global writes (e.g. the pre-compress own-block max slot) before arriving
+    const unsigned prev = atomicAdd(&s_bar_arrived[k], 1u);
     const uint64_t t0 = globaltimer();
-    for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->bar)) < target; ++it) {
-      __nanosleep(64);
-      if ((it & 63u) == 0) {
-        if (aborted(P, ctl)) {
-          latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, abort_detail(ctl, R.rank));
-          ok = 0;
-          break;
-        }
-        if (globaltimer() - t0 > P.timeout_ns) {
-          latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, 0);
-          broadcast_abort(P, R);
-          ok = 0;
-          break;
+    if (prev == (unsigned)kWarps - 1) {  // last warp of the CTA: the CTA's global arrival
+      atomicMax(&cb(ctl)->maxslot[k], ((unsigned long long)s_seq << 32) | *(volatile unsigned*)&s_bar_max[k]);
+      __threadfence();
+      atomicAdd(&cb(ctl)->bar, 1ull);
+      const unsigned long long target = (unsigned long long)(k + 1) * P.G;
+      for (uint32_t it = 1; ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->bar)) < target; ++it) {
+        __nanosleep(32);
+        if ((it & 63u) == 0) {
+          if (aborted(P, ctl)) {
+            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, abort_detail(ctl, R.rank));
+            ok = 0;
+            break;
+          }
+          if (globaltimer() - t0 > P.timeout_ns) {
+            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, 0);
+            broadcast_abort(P, R);
+            ok = 0;
+            break;
+          }
         }
       }
+      const unsigned long long w = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->maxslot[k]));
+      v = ((uint32_t)(w >> 32) == s_seq) ? __uint_as_float((uint32_t)w) : 0.f;
+      *(volatile float*)&s_bar_vmax[k] = v;
+      __threadfence_block();
+      *(volatile int*)&s_bar_open[k] = ok ? 1 : 2;
+    } else {
+      int st;
+      for (uint32_t it = 1; (st = *(volatile int*)&s_bar_open[k]) == 0; ++it) {
+        __nanosleep(32);
+        if ((it & 63u) == 0) {
+          if (aborted(P, ctl)) {
+            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, abort_detail(ctl, R.rank));
+            st = 2;
+            break;
+          }
+          if (globaltimer() - t0 > P.timeout_ns) {
+            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, 0);
+            broadcast_abort(P, R);
+            st = 2;
+            break;
+          }
+        }
+      }
+      __threadfence_block();
+      ok = st == 1;
+      v = *(volatile float*)&s_bar_vmax[k];
     }
-    const unsigned long long w = ld_acquire_gpu(reinterpret_cast<uint64_t*>(&cb(ctl)->maxslot[k]));
-    v = ((uint32_t)(w >> 32) == s_seq) ? __uint_as_float((uint32_t)w) : 0.f;
   }
   __syncwarp();
   ok = __shfl_sync(0xffffffffu, ok, 0);
@@ -969,6 +1012,7 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     uint32_t it = P.iteration;
     if (P.iteration_dev != nullptr) it = ld_relaxed_gpu_u32(P.iteration_dev);
     s_iter = it;
+    for (int i = 0; i < kMaxBarriers; ++i) s_bar_arrived[i] = 0, s_bar_max[i] = 0, s_bar_open[i] = 0;
     if (blockIdx.x % P.G == 0) {  // the next call's bank starts from zero
       CtlBank* nb = &ctl->bank[(calls + 1) & 1];
       nb->bar = 0;

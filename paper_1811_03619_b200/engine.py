@@ -726,18 +726,22 @@ class RankEngine:
 # iteration's forward/backward, and the ring's resident CTAs (most of them
 # waiting on flags) keep SMs from the compute kernels: for a small gradient
 # the budget is cut to 64 CTAs (C1 MLP, N = 4: 6067 -> 7602 iterations/s at
-# 256 -> 64; compute 143 -> 110 us per step), while a large one is best
-# finished fast (C3 AlexNet: 185.4 / 191.7 / 195.1 / 197.4 iterations/s at
-# 64 / 256 / 384 / 592 CTAs; C2, C4: flat) -- profiles/r02/engine_ctas/.
+# 256 -> 64; compute 143 -> 110 us per step); a large one gets 256 (C3
+# AlexNet: 185.4 / 191.7 / 195.1 / 197.4 iterations/s at 64 / 256 / 384 / 592
+# CTAs, but at 592 the ring holds every register of every SM and the next
+# iteration's compute no longer overlaps it at all -- the pipeline's
+# contract, tests/test_gpu_engine.py -- so Pipe-SGD stops at 256; C2, C4:
+# flat) -- profiles/r02/engine_ctas/.
 COMM_CTAS = 0
 PIPE_SMALL_GRADIENT_CTAS = 64
+PIPE_LARGE_GRADIENT_CTAS = 256
 SMALL_GRADIENT_BYTES = 32 << 20
 
 
 def default_comm_ctas(mode: str, num_params: int) -> int:
     """The ring's CTA budget for a training run (see COMM_CTAS)."""
-    if mode == MODE_PIPE_SGD and 4 * num_params <= SMALL_GRADIENT_BYTES:
-        return PIPE_SMALL_GRADIENT_CTAS
+    if mode == MODE_PIPE_SGD:
+        return PIPE_SMALL_GRADIENT_CTAS if 4 * num_params <= SMALL_GRADIENT_BYTES else PIPE_LARGE_GRADIENT_CTAS
     return COMM_CTAS
 
 
