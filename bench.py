@@ -929,6 +929,8 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
     out["measured_step_ms"] = step_ms
     out["eq4_over_measured"] = out["eq4_pipe_ms"] / step_ms
     out["bound"] = "compute" if upd + comp >= comm else "communication"
+    if upd + comp > 0:
+        out["eq7_scaling_efficiency"] = T.scaling_efficiency(stages)  # busy / max(busy, comm), timing.py:191-200
     if not (allreduce and N > 1 and calib and probes):
         return out
     a, b, S = max(0.0, calib["alpha_s"]), calib["beta_s_per_byte"], probes["S_s"]

@@ -88,3 +88,20 @@ def test_matches_reference_on_random_parameters():
             assert T.scaling_efficiency(ours_s) == pytest.approx(R.scaling_efficiency(ref_s), rel=1e-12)
         a, b = T.recommend_config(ours_s, ours_c), R.recommend_config(ref_s, ref_c)
         assert (a.depth, a.comm_mode, a.bound) == (b.depth, b.comm_mode, b.bound)
+
+
+def test_compare_ring_eq5_terms_and_quant8_extension():
+    """timing.compare_ring: Eq. 5's four terms (timing.py:119-132) for the
+    codec's payload bytes, the 25 % flag of compare_prediction
+    (harness.py:687-720), and the quant8-only extension terms."""
+    from paper_1811_03619_b200 import timing as T
+    p, n = 4, 1_000_000
+    a, b, g, S, d = 2e-6, 1 / 700e9, 1 / 400e9, 5e-6, 1e-11
+    for codec, w in (("none", 4), ("trunc16", 2), ("quant8", 1)):
+        nb = n * w
+        eq5 = 2 * (p - 1) * a + 2 * (p - 1) / p * nb * b + (p - 1) / p * nb * g + S
+        row = T.compare_ring(eq5, p, codec, n, a, b, g, S, d)
+        assert abs(row["eq5_ms"] - eq5 * 1e3) < 1e-12 and not row["flagged"]
+        ext = eq5 + ((nb / p * g + (p - 1) / p * n * d) if codec == "quant8" else 0.0)
+        assert abs(row["eq5_ext_ms"] - ext * 1e3) < 1e-12
+        assert T.compare_ring(eq5 * 1.3, p, codec, n, a, b, g, S, d)["flagged"]
