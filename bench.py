@@ -437,6 +437,11 @@ def our_arm(args, ws, rank, local):
         return bufs["x"][b], bufs["y"][b]
 
     eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True, fused=bool(args.fused))
+    comm_sms = int(os.environ.get("BENCH_COMM_SMS", "0"))
+    if comm_sms:  # experiment: the comm stream on a green-context SM partition
+        from paper_1811_03619_b200.greenctx import green_stream
+        eng.ms, got = green_stream(local, comm_sms)
+        print(f"comm stream on a green context of {got} SMs", file=sys.stderr)
     loss_host = torch.zeros(total_steps + 2, dtype=torch.float32).pin_memory()
     nb = eng.K if eng.K >= 2 else 1  # buffer index == graph parity
     bufs.update(nb=nb, x=[x_dev.clone() for _ in range(nb)], y=[y_dev.clone() for _ in range(nb)],
