@@ -54,8 +54,13 @@ def parse():
     ap.add_argument("--global-batch", type=int, default=None,
                     help="default: the paper's global batch for the config (100 MNIST, 512 CIFAR, 256 ImageNet)")
     ap.add_argument("--ctas", type=int, default=-1,
-                    help="128-thread CTAs the ring kernel may occupy per GPU (-1: engine.default_comm_ctas -- "
-                         "Pipe-SGD 64 on gradients <= 32 MB else 256, D-Sync every SM; 0: every SM)")
+                    help="128-thread CTAs the ring kernel may occupy per GPU (-1: engine.default_comm_partition "
+                         "-- Pipe-SGD 64 on gradients <= 8 MB else 4 per partition SM, D-Sync every SM; "
+                         "0: every SM)")
+    ap.add_argument("--comm-sms", type=int, default=-1,
+                    help="SMs of the green-context partition the comm stream runs in (-1: "
+                         "engine.default_comm_partition -- Pipe-SGD at N > 1: 32 on gradients of 8-32 MB, 48 above; "
+                         "0: no partition)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
                     help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync, fused)")
@@ -377,6 +382,7 @@ def workload_config(args, n, N):
             "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
             "cuda_graphs": bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused),
             "ring_ctas": args.ctas if args.ctas > 0 else None,
+            "comm_partition_sms": args.comm_sms or None,
             "model_math": "fp32 (TF32 disabled for cuDNN convolutions and cuBLAS matmuls)",
             "l2": "not flushed: each step streams the model's activations for the per-GPU batch plus the "
                   "gradient, weights and slots through HBM"}
@@ -401,9 +407,12 @@ def our_arm(args, ws, rank, local):
     fm = FlatModel(mod, dev)
     n = fm.num_params
     cap = max(n, 1 << 26) if N > 1 else (n if args.mode == "ps_sync" else 1 << 10)
+    from paper_1811_03619_b200.engine import default_comm_ctas, default_comm_partition
+    part_sms, part_ctas = default_comm_partition(args.mode, n, N)
+    if args.comm_sms < 0:
+        args.comm_sms = part_sms
     if args.ctas < 0:
-        from paper_1811_03619_b200.engine import default_comm_ctas
-        args.ctas = default_comm_ctas(args.mode, n)
+        args.ctas = part_ctas if args.comm_sms else default_comm_ctas(args.mode, n)
     if N > 1:
         ep = ProcessGroupTransport.endpoint(local, max_elems=cap, ctas=args.ctas, timeout_s=60.0)
     else:
@@ -436,12 +445,8 @@ def our_arm(args, ws, rank, local):
             eng.cs.wait_event(bufs["copied"][b])
         return bufs["x"][b], bufs["y"][b]
 
-    eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True, fused=bool(args.fused))
-    comm_sms = int(os.environ.get("BENCH_COMM_SMS", "0"))
-    if comm_sms:  # experiment: the comm stream on a green-context SM partition
-        from paper_1811_03619_b200.greenctx import green_stream
-        eng.ms, got = green_stream(local, comm_sms)
-        print(f"comm stream on a green context of {got} SMs", file=sys.stderr)
+    eng = RankEngine(rank, N, ep, fm, cfg, batch_fn, trace=True, fused=bool(args.fused), comm_sms=args.comm_sms)
+    args.comm_sms = eng.comm_sms  # the partition actually made (0 = none / unavailable)
     loss_host = torch.zeros(total_steps + 2, dtype=torch.float32).pin_memory()
     nb = eng.K if eng.K >= 2 else 1  # buffer index == graph parity
     bufs.update(nb=nb, x=[x_dev.clone() for _ in range(nb)], y=[y_dev.clone() for _ in range(nb)],

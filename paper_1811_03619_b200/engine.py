@@ -202,7 +202,7 @@ class RankEngine:
     """One rank's Pipe-SGD loop on one GPU (enqueue-only host thread)."""
 
     def __init__(self, rank: int, world: int, endpoint: GpuEndpoint, fm: FlatModel, config: RunConfig,
-                 batch_fn: BatchFn, trace: bool = True, grad_fn=None, fused: bool = True):
+                 batch_fn: BatchFn, trace: bool = True, grad_fn=None, fused: bool = True, comm_sms: int = 0):
         """fused=True (default): the comm stream runs ONE kernel per iteration —
         the ring with the local pre-compress applied on load and the pipe
         re-compress written as the slot by its allgather (gp_allreduce_ex);
@@ -218,6 +218,20 @@ class RankEngine:
         # comm stream priority (PIPESGD_COMM_PRIORITY, lower = higher; 0 = same
         # as compute): its CTAs are scheduled ahead of compute CTAs as SMs free up
         self.ms = torch.cuda.Stream(self.dev, priority=int(os.environ.get("PIPESGD_COMM_PRIORITY", "0")))
+        # comm_sms > 0: the comm stream lives in a green context of that many
+        # SMs (greenctx.py), so the pipelined ring occupies a fixed slice of
+        # the GPU; the communicator's CTA budget must fit it (4 CTAs per SM)
+        self.comm_sms = 0
+        if comm_sms > 0:
+            from .greenctx import green_stream
+            try:
+                self.ms, self.comm_sms = green_stream(self.dev.index, comm_sms)
+            except Exception as err:  # noqa: BLE001 - no green contexts: plain stream, full budget
+                import warnings
+                warnings.warn(f"green context unavailable ({err}); the comm stream shares every SM")
+            if self.comm_sms and world > 1 and endpoint.info()["ctas"] > 4 * self.comm_sms:
+                raise ConfigError(f"ring CTA budget {endpoint.info()['ctas']} exceeds the {self.comm_sms}-SM "
+                                  f"comm partition ({4 * self.comm_sms} resident CTAs)")
         self.tracing = trace
         self.events: list = []  # (iteration, stage, ev0, ev1, consumed)
         K = max(config.depth, 1)
@@ -720,29 +734,52 @@ class RankEngine:
 
 # ----------------------------------------------------------------- clusters
 
-# CTAs (128 threads each) the ring kernel may occupy; 0 = the communicator's
-# default, every SM (4 CTAs per SM). D-Sync runs the ring between computes:
-# the full budget gives the shortest ring. Pipe-SGD runs it beside the next
-# iteration's forward/backward, and the ring's resident CTAs (most of them
-# waiting on flags) keep SMs from the compute kernels: for a small gradient
-# the budget is cut to 64 CTAs (C1 MLP, N = 4: 6067 -> 7602 iterations/s at
-# 256 -> 64; compute 143 -> 110 us per step); a large one gets 256 (C3
-# AlexNet: 185.4 / 191.7 / 195.1 / 197.4 iterations/s at 64 / 256 / 384 / 592
-# CTAs, but at 592 the ring holds every register of every SM and the next
-# iteration's compute no longer overlaps it at all -- the pipeline's
-# contract, tests/test_gpu_engine.py -- so Pipe-SGD stops at 256; C2, C4:
-# flat) -- profiles/r02/engine_ctas/.
+# Where the ring runs. D-Sync runs it between computes: every SM (CTA budget
+# 0 = the communicator's default, 4 CTAs per SM) gives the shortest ring.
+# Pipe-SGD runs it beside the next iteration's forward/backward, and the
+# ring's resident CTAs (most of them waiting on flags) keep SMs from the
+# compute kernels:
+#   * a small gradient (<= 8 MB) gets 64 CTAs on the shared GPU (C1 MLP,
+#     N = 4: 6067 -> 7602 iterations/s from 256 to 64 CTAs; compute 143 ->
+#     110 us per step; a 16-SM partition slows its latency-bound LL ring
+#     and the end-to-end rate);
+#   * up to 32 MB the comm stream runs in a green-context partition of 32
+#     SMs with 128 CTAs (C2 CNN, N = 4: 661.8 at 64 CTAs on every SM ->
+#     683.0; 16 SMs: 629.4);
+#   * a large one gets 48 SMs with 192 CTAs (C3 AlexNet, N = 4: 191.5 at 256
+#     CTAs spread over every SM -> 198.1, compute 5.04 -> 4.84 ms per step;
+#     592 CTAs on every SM gave 197.4 but held every register of every SM,
+#     so the next compute no longer overlapped the ring -- not the paper's
+#     pipeline). One rank (no ring): C3 58.1 either way, no partition.
+# profiles/r02/engine_ctas/, profiles/r02/green_ctx/.
 COMM_CTAS = 0
 PIPE_SMALL_GRADIENT_CTAS = 64
-PIPE_LARGE_GRADIENT_CTAS = 256
-SMALL_GRADIENT_BYTES = 32 << 20
+PIPE_MID_GRADIENT_SMS = 32
+PIPE_LARGE_GRADIENT_SMS = 48
+PIPE_LARGE_GRADIENT_CTAS = 256  # no partition (one rank, or GPUs shared by ranks)
+SMALL_GRADIENT_BYTES = 8 << 20
+MID_GRADIENT_BYTES = 32 << 20
+
+
+def default_comm_partition(mode: str, num_params: int, world: int = 2) -> tuple[int, int]:
+    """(green-context SMs for the comm stream, 0 = shared GPU; ring CTA budget,
+    0 = every SM) for a training run with one rank per GPU (see COMM_CTAS).
+    One rank has no ring to fence off: no partition."""
+    if mode == MODE_PIPE_SGD:
+        if 4 * num_params <= SMALL_GRADIENT_BYTES:
+            return 0, PIPE_SMALL_GRADIENT_CTAS
+        if world < 2:
+            return 0, PIPE_SMALL_GRADIENT_CTAS if 4 * num_params <= MID_GRADIENT_BYTES else PIPE_LARGE_GRADIENT_CTAS
+        sms = PIPE_MID_GRADIENT_SMS if 4 * num_params <= MID_GRADIENT_BYTES else PIPE_LARGE_GRADIENT_SMS
+        return sms, 4 * sms
+    return 0, COMM_CTAS
 
 
 def default_comm_ctas(mode: str, num_params: int) -> int:
-    """The ring's CTA budget for a training run (see COMM_CTAS)."""
-    if mode == MODE_PIPE_SGD:
-        return PIPE_SMALL_GRADIENT_CTAS if 4 * num_params <= SMALL_GRADIENT_BYTES else PIPE_LARGE_GRADIENT_CTAS
-    return COMM_CTAS
+    """The ring's CTA budget without a partition (one rank, or GPUs shared by
+    several ranks): Pipe-SGD keeps a gradient <= 32 MB to 64 CTAs and spreads
+    256 CTAs of a larger one over every SM."""
+    return default_comm_partition(mode, num_params, 1)[1]
 
 
 def _make_transport(workers: int, timeout_s: float, max_elems: int, ctas: int = COMM_CTAS):
@@ -769,14 +806,17 @@ class DeviceDataset:
 def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_s: float = 0.0,
                        byte_time_s: float = 0.0, batch_provider=None, timeout_s: float = 30.0,
                        transport=None, grad_fn=None, trace: bool = True, fused: bool = True,
-                       comm_ctas: int | None = None) -> list[WorkerResult]:
+                       comm_ctas: int | None = None, comm_sms: int | None = None) -> list[WorkerResult]:
     """Run a full training job with all ranks as threads of this process
     (engine.py:563-618), one GPU per rank (GpuTransport) or all ranks on one
     GPU (EmulatedTransport) when there are fewer GPUs than workers.
 
     `model` is a ModelSpec (logistic / MLP, reference layout and init);
     `grad_fn(rank, t, params) -> (loss, grad)` optionally replaces the model's
-    forward/backward (used by parity tests to inject oracle gradients)."""
+    forward/backward (used by parity tests to inject oracle gradients).
+    comm_ctas / comm_sms (None = default_comm_partition, applied only when
+    this call makes one GpuTransport rank per GPU): the ring's CTA budget and
+    the green-context SMs of the comm stream."""
     if workers < 1:
         raise ConfigError("need at least one worker")
     if latency_s or byte_time_s:
@@ -785,8 +825,12 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
         model = ModelSpec(model.kind, tuple(model.layer_dims))
     n = model.num_params
     own_transport = transport is None
+    one_per_gpu = transport is None and torch.cuda.device_count() >= workers
+    part_sms, part_ctas = default_comm_partition(config.mode, n, workers)
+    if comm_sms is None:
+        comm_sms = part_sms if one_per_gpu else 0
     if comm_ctas is None:
-        comm_ctas = default_comm_ctas(config.mode, n)
+        comm_ctas = part_ctas if comm_sms else default_comm_ctas(config.mode, n)
     tr = transport or _make_transport(workers, timeout_s, max(n, 1), comm_ctas)
     shards = [np.arange(r % workers, dataset.features.shape[0], workers) for r in range(workers)]
     if batch_provider is None and grad_fn is None:
@@ -812,7 +856,8 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
                         shards[rank][rng.choice(len(shards[rank]), size=config.batch_size, replace=False)]
                     return data.gather(idx)
 
-                eng = RankEngine(r, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn, fused=fused)
+                eng = RankEngine(r, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn, fused=fused,
+                                 comm_sms=comm_sms if isinstance(tr, GpuTransport) else 0)
                 ipe = max(1, len(shards[r]) // config.batch_size)
                 torch.cuda.synchronize(dev)
                 barrier.wait()
@@ -851,12 +896,13 @@ def run_inproc_cluster(workers: int, config: RunConfig, dataset, model, latency_
 
 def run_process_worker(config: RunConfig, dataset, model, timeout_s: float = 30.0, batch_provider=None,
                        grad_fn=None, trace: bool = True, fused: bool = True, comm_ctas: int | None = None,
-                       group=None) -> WorkerResult:
+                       comm_sms: int | None = None, group=None) -> WorkerResult:
     """One rank of a multi-process run (one process per GPU under torchrun):
     the analogue of the reference's run_tcp_worker (engine.py:621-646).
     torch.distributed must be initialised; the rank's GPU is LOCAL_RANK.
     Ranks exchange inbox IPC handles once over the process group, then the
-    ring moves gradients over NVLink only."""
+    ring moves gradients over NVLink only. comm_ctas / comm_sms: as in
+    run_inproc_cluster (None = default_comm_partition)."""
     import os
 
     import torch.distributed as dist
@@ -870,9 +916,13 @@ def run_process_worker(config: RunConfig, dataset, model, timeout_s: float = 30.
     torch.cuda.set_device(local)
     if not isinstance(model, ModelSpec):
         model = ModelSpec(model.kind, tuple(model.layer_dims))
+    part_sms, part_ctas = default_comm_partition(config.mode, model.num_params, workers)
+    if comm_sms is None:
+        comm_sms = part_sms
+    if comm_ctas is None:
+        comm_ctas = part_ctas if comm_sms else default_comm_ctas(config.mode, model.num_params)
     ep = ProcessGroupTransport.endpoint(local, group=group, timeout_s=timeout_s,
-                                        max_elems=max(model.num_params, 1),
-                                        ctas=comm_ctas or default_comm_ctas(config.mode, model.num_params))
+                                        max_elems=max(model.num_params, 1), ctas=comm_ctas)
     dev = ep.device
     shard = np.arange(rank % workers, dataset.features.shape[0], workers)
     if batch_provider is None and grad_fn is None and config.batch_size > len(shard):
@@ -887,7 +937,8 @@ def run_process_worker(config: RunConfig, dataset, model, timeout_s: float = 30.
                 shard[rng.choice(len(shard), size=config.batch_size, replace=False)]
             return data.gather(idx)
 
-        eng = RankEngine(rank, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn, fused=fused)
+        eng = RankEngine(rank, workers, ep, fm, config, batch_fn, trace=trace, grad_fn=grad_fn, fused=fused,
+                         comm_sms=comm_sms)
         torch.cuda.synchronize(dev)
         dist.barrier(group)
         start = torch.cuda.Event(enable_timing=True)

@@ -1,23 +1,47 @@
 """An SM partition for the comm stream (CUDA green contexts): the ring kernel
 launched on this stream runs only on its `sms` SMs, so the pipelined ring
 takes a fixed slice of the GPU instead of spreading its resident CTAs over
-every SM beside the next iteration's compute. Experimental (bench knob
-BENCH_COMM_SMS); driver API through cuda-python."""
+every SM beside the next iteration's compute (RankEngine comm_sms,
+engine.default_comm_partition). Kernels of the primary context (the
+forward/backward) still run on every SM. Driver API through cuda-python;
+one green context + stream per (device, SM count) per process."""
 
 from __future__ import annotations
 
+import threading
+
 
 def _check(res, what):
-    err = res[0] if isinstance(res, tuple) else res
-    if int(err) != 0:
-        raise RuntimeError(f"{what} failed: {err}")
-    return res[1:] if isinstance(res, tuple) and len(res) > 2 else (res[1] if isinstance(res, tuple) else None)
+    """cuda-python returns (err,) or (err, value) or (err, v1, v2, ...)."""
+    res = res if isinstance(res, tuple) else (res,)
+    if int(res[0]) != 0:
+        raise RuntimeError(f"{what} failed: {res[0]}")
+    return None if len(res) == 1 else (res[1] if len(res) == 2 else res[1:])
+
+
+_CONTEXTS: dict = {}
+_LOCK = threading.Lock()
 
 
 def green_stream(device_index: int, sms: int):
-    """A torch ExternalStream bound to a green context of `sms` SMs (the
-    driver may round up to its SM granularity). Returns (stream, sm_count)."""
+    """A new torch ExternalStream bound to a green context of `sms` SMs (the
+    driver may round up to its SM granularity). Returns (stream, sm_count).
+    The green context is made once per (device, SM count) and shared; every
+    call gets its own stream (ranks sharing a GPU must not share one)."""
     import torch
+    from cuda.bindings import driver as d
+
+    key = (int(device_index), int(sms))
+    with _LOCK:
+        if key not in _CONTEXTS:
+            _CONTEXTS[key] = _make_green_ctx(*key)
+        gctx, count = _CONTEXTS[key]
+    st = _check(d.cuGreenCtxStreamCreate(gctx, d.CUstream_flags.CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate")
+    stream = torch.cuda.ExternalStream(int(st), device=torch.device("cuda", device_index))
+    return stream, count
+
+
+def _make_green_ctx(device_index: int, sms: int):
     from cuda.bindings import driver as d
 
     _check(d.cuInit(0), "cuInit")
@@ -26,12 +50,9 @@ def green_stream(device_index: int, sms: int):
     out = d.cuDevSmResourceSplitByCount(1, res, 0, sms)
     if int(out[0]) != 0:
         raise RuntimeError(f"cuDevSmResourceSplitByCount failed: {out[0]}")
-    groups, n_groups = out[1], out[2]
+    groups = out[1]
     desc = _check(d.cuDevResourceGenerateDesc(groups, 1), "cuDevResourceGenerateDesc")
     gctx = _check(d.cuGreenCtxCreate(desc, dev, d.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM),
                   "cuGreenCtxCreate")
-    st = _check(d.cuGreenCtxStreamCreate(gctx, d.CUstream_flags.CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate")
     count = groups[0].sm.smCount if hasattr(groups[0], "sm") else sms
-    stream = torch.cuda.ExternalStream(int(st), device=torch.device("cuda", device_index))
-    stream._green_ctx = gctx  # keep alive
-    return stream, int(count)
+    return gctx, int(count)

@@ -151,6 +151,64 @@ def test_allreduce_overlaps_next_iteration_compute(P):
     assert cand > 10 and ov >= cand * 0.5, (ov, cand)
 
 
+@pytest.mark.parametrize("codec", [0, 2])
+def test_comm_partition_is_bit_exact(P, codec):
+    """The comm stream on a green-context SM partition (RankEngine comm_sms,
+    engine.default_comm_partition) changes where the ring runs, not what it
+    computes: weights bit-identical to the unpartitioned engine, and the
+    partition is really made (one GPU per rank, or both ranks sharing one)."""
+    from helpers import real_transport, run_ranks
+    from paper_1811_03619_b200.engine import RankEngine, RunConfig
+    from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
+    spec = ModelSpec("mlp", (64, 256, 10))
+    p, T = 2, 8
+
+    def train(sms):
+        tr = real_transport(P, p, timeout_s=30.0, max_elems=spec.num_params, ctas=32)
+
+        def op(r, ep):
+            dev = ep.device
+            with torch.cuda.device(dev):
+                fm = FlatModel(SpecNet(spec), dev, init_params(spec, 1))
+                g = torch.Generator(device="cpu").manual_seed(20 + r)
+                x = torch.randn(32, 64, generator=g).to(dev)
+                y = torch.randint(0, 10, (32,), generator=g).to(dev)
+                cfg = RunConfig(mode="pipe_sgd", iterations=T, learning_rate=0.05, codec=codec, batch_size=32)
+                eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False, comm_sms=sms)
+                eng.run()
+                eng.cs.synchronize()
+                eng.ms.synchronize()
+                ep._check_errors(fm.num_params)
+                return fm.params.cpu().numpy(), eng.comm_sms
+
+        try:
+            return run_ranks(tr, op)
+        finally:
+            tr.close()
+
+    plain, part = train(0), train(16)
+    for r in range(p):
+        assert part[r][1] >= 16, "no green-context partition was made"
+        assert_bits_equal(part[r][0], plain[r][0], f"rank {r} codec {codec}")
+
+
+def test_comm_partition_rejects_budget_beyond_partition(P):
+    from helpers import real_transport
+    from paper_1811_03619_b200.engine import ConfigError, RankEngine, RunConfig
+    from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
+    spec = ModelSpec("mlp", (8, 16, 3))
+    tr = real_transport(P, 2, timeout_s=10.0, max_elems=spec.num_params, ctas=256)
+    try:
+        ep = tr.endpoint(0)
+        with torch.cuda.device(ep.device):
+            fm = FlatModel(SpecNet(spec), ep.device, init_params(spec, 1))
+            with pytest.raises(ConfigError, match="partition"):
+                RankEngine(0, 2, ep, fm, RunConfig(mode="pipe_sgd", iterations=2, batch_size=4), lambda r, t: None,
+                           trace=False, comm_sms=16)
+    finally:
+        tr.close()
+
+
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_run_process_worker_under_torchrun_bit_exact():
     """One process per GPU (torchrun, CUDA IPC inboxes): run_process_worker

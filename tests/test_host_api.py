@@ -138,3 +138,19 @@ def test_wire_and_payload_sizes_match_reference(codec):
             assert ref.payload_size(rc, n) == payload_size(c, n)
     with pytest.raises(CodecError):
         payload_size(c, -1)
+
+
+def test_default_comm_partition_policy():
+    """engine.default_comm_partition: D-Sync rings on every SM; Pipe-SGD keeps
+    a small gradient's ring to 64 CTAs on the shared GPU and fences a large
+    mid-size one into a 32-SM green context and a large one into 48 SMs (4
+    CTAs per SM) when there is a ring."""
+    from paper_1811_03619_b200.engine import default_comm_ctas, default_comm_partition
+    assert default_comm_partition("d_sync", 61_100_840, 4) == (0, 0)
+    assert default_comm_partition("pipe_sgd", 648_010, 4) == (0, 64)
+    assert default_comm_partition("pipe_sgd", 61_100_840, 4) == (48, 192)
+    assert default_comm_partition("pipe_sgd", 4_700_000, 4) == (32, 128)
+    assert default_comm_partition("pipe_sgd", 61_100_840, 1) == (0, 256)
+    assert default_comm_ctas("pipe_sgd", 61_100_840) == 256
+    assert default_comm_ctas("pipe_sgd", 648_010) == 64
+    assert default_comm_ctas("pipe_sgd", 4_700_000) == 64

@@ -11,4 +11,4 @@ run() {  # sms ctas graphs
 run 16 64 0
 run 16 64 1
 run 32 128 1
-run 0 256 1
+
