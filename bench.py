@@ -465,13 +465,13 @@ def our_arm(args, ws, rank, local):
         copy_stream.wait_event(bufs["free"][b])
         if copy_after_ring and pipe and "graphs" in bufs and tt - 2 in eng.graph_ready_tag.values():
             copy_stream.wait_event(eng.ev_agg[(tt - 2) % eng.K])
-        c0 = torch.cuda.Event(enable_timing=True)
+        c0 = pool.pop() if pool else torch.cuda.Event(enable_timing=True)
         c0.record(copy_stream)
         with torch.cuda.stream(copy_stream):
             bufs["x"][b].copy_(x_host, non_blocking=True)
             bufs["y"][b].copy_(y_host, non_blocking=True)
         bufs["copied"][b].record(copy_stream)
-        c1 = torch.cuda.Event(enable_timing=True)
+        c1 = pool.pop() if pool else torch.cuda.Event(enable_timing=True)
         c1.record(copy_stream)
         copy_events.append((c0, c1))
 
@@ -479,8 +479,14 @@ def our_arm(args, ws, rank, local):
         if N > 1:
             dist.barrier()
 
+    host_ms = {}  # host enqueue time per step (ms), resident / e2e
+    pool = []  # timing events made before the timed region (host time inside it is the step's budget)
+
     def timed_region(t0, steps, e2e):
         mode["e2e"] = e2e
+        eng.reserve_events(8 * steps + 16)
+        pool[:] = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 4)]
+        done_evs = [torch.cuda.Event() for _ in range(steps)]
         torch.cuda.synchronize(dev)
         barrier()
         eng.events.clear()
@@ -491,15 +497,17 @@ def our_arm(args, ws, rank, local):
         if e2e:
             copy_stream.wait_stream(eng.cs)
             prefetch(t0)
+        h0 = time.perf_counter()
         for t in range(t0, t0 + steps):
             step(t)
             if e2e:  # device->host read of the step's loss (async into pinned memory), on its own
                 # stream after the step so the next step's kernels do not queue behind the PCIe read
-                done = torch.cuda.Event()
+                done = done_evs[t - t0]
                 done.record(eng.cs)
                 d2h_stream.wait_event(done)
                 with torch.cuda.stream(d2h_stream):
                     loss_host[t:t + 1].copy_(eng.losses[t:t + 1], non_blocking=True)
+        host_ms[e2e] = (time.perf_counter() - h0) * 1e3 / steps
         ends = []
         for st in (eng.cs, eng.ms, d2h_stream):
             e = torch.cuda.Event(enable_timing=True)
@@ -695,8 +703,12 @@ def our_arm(args, ws, rank, local):
         from paper_1811_03619_b200 import timing as T
         S = max_over_ranks(T.barrier_time(ep), dev)
         g = ep.info()["ctas"]  # the probes run on the ring's own thread budget
-        probes = {"S_s": S}
+        # the smallest real call (16 elements per rank, codec none): calibrates
+        # the per-call cost Eq. 5 has no term for (timing.ring_fixed_overhead)
+        small = ring_vs_nccl(ep, "none", N, dev, [16 * N])[0]
+        probes = {"S_s": S, "small_call_s": small["none"]["ms"] * 1e-3, "small_n": 16 * N}
         if rank == 0:
+            probes["gamma_small"] = T.gamma_hop("none", 16, dev, ring_ctas=g)
             for key, m in (("1k", 1024), ("mid", n), ("big", 1 << 26)):
                 probes["gamma_" + key] = T.gamma_hop(args.codec, max(1, m // N), dev, ring_ctas=g)
                 probes["delta_" + key] = T.delta_decode(args.codec, max(1, m // N), dev)
@@ -712,11 +724,13 @@ def our_arm(args, ws, rank, local):
                 "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": h2d * N,
                         "d2h_bytes_per_step": 4 * N,
                         "h2d_copy_ms_avg": float(np.mean(copy_ms)) if copy_ms else None,
+                        "host_enqueue_ms_per_step": host_ms.get(True),
                         "streams": streams,
                         "how": "same engine; every step copies the rank's batch from pinned host memory (on a "
                                "copy stream into a per-parity buffer, overlapping the previous step's compute) "
                                "and reads its loss back into pinned memory (on a D2H stream after the step)"},
                 "gpu_launches": per_iter_launches * args.steps,
+                "host_enqueue_ms_per_step": host_ms.get(False),
                 "roofline": roof, "kernels": kernels, "clocks": clk.summary(),
                 "samples_per_s": value * args.global_batch}
         if allreduce:
@@ -944,10 +958,11 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
     if not (allreduce and N > 1 and calib and probes):
         return out
     a, b, S = max(0.0, calib["alpha_s"]), calib["beta_s_per_byte"], probes["S_s"]
+    fixed = T.ring_fixed_overhead(probes["small_call_s"], N, probes["small_n"], a, b, probes["gamma_small"], S)
     rows = []
     for row, key in zip(allreduce, ("1k", "mid", "big")):
         rows.append(T.compare_ring(row[codec]["ms"] * 1e-3, N, codec, row["n"], a, b, probes["gamma_" + key], S,
-                                   probes["delta_" + key]))
+                                   probes["delta_" + key], fixed_s=fixed))
     mid = rows[1]
     gam = probes["gamma_mid"]
     cluster = T.ClusterParams(workers=N, latency_s=a, byte_time_s=b, reduce_time_s=gam, sync_time_s=S,
@@ -961,8 +976,10 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
                     "gamma_gbs": 1 / gam / 1e9 if gam else None, "S_us": S * 1e6},
         "rings": rows, "step_gradient_ring": mid,
         "note": "measured = the same ring alone, back-to-back, at the engine's CTA budget (the allreduce rows); "
-                "gamma is one fused hop on one GPU on that same budget; eq5_ext adds the step-0 encode and the "
-                "allgather decode the paper's model leaves out (timing.compare_ring)"}
+                "gamma is one fused hop on one GPU on that same budget; eq5_ext adds the step-0 encode, the "
+                "allgather decode and the per-call fixed cost (launch, call open / close: Eq. 5's residual on a "
+                "16-element-per-rank call) the paper's model leaves out (timing.compare_ring)",
+        "fixed_per_call_us": fixed * 1e6}
     out["compare_prediction"] = [{"mode": mode, "measured_ms": step_ms, "predicted_ms": pred_it * 1e3,
                                   "rel_error": rel, "flagged": abs(rel) > 0.25,
                                   "bound": "communication" if T.ring_comm_time(cluster) > (upd + comp) / 1e3

@@ -108,6 +108,11 @@ int gp_comm_set_trace(gp_comm* comm, void* device_buffer);
  * carries and checks the real step t on every replay (the host writes t
  * before each replay). NULL restores the argument. */
 int gp_comm_set_iteration_source(gp_comm* comm, const uint32_t* device_tag);
+/* Wire protocol cap (NCCL_PROTO-like; every rank must pass the same value):
+ * the LL protocol only for blocks whose payload is at most ll_max_bytes
+ * (and the library's own 2 MiB limit); 0 = flag protocol for every call.
+ * Default: no cap. Results are bit-identical either way. */
+int gp_comm_set_protocol(gp_comm* comm, uint64_t ll_max_bytes);
 int gp_comm_info(gp_comm* comm, int64_t* out /* [rank, world, device, max_elems, ctas, inbox_bytes, seq, mode (0 own GPU, 1 emulated, 2 per-rank launch on a shared GPU)] */);
 int gp_comm_destroy(gp_comm* comm);
 /* Test hook: set the device call counter of this communicator's inbox(es)

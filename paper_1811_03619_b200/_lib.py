@@ -24,7 +24,7 @@ GP_RING_PRECOMPRESS, GP_RING_SLOT_OUT = 1, 2
 # Every symbol include/pipesgd.h declares (checked by tests/test_cabi.py).
 EXPORTS = (
     "gp_comm_create", "gp_comm_create_emulated", "gp_comm_ipc_handle", "gp_comm_connect_ipc",
-    "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_set_iteration_source", "gp_comm_info", "gp_comm_destroy",
+    "gp_comm_connect_local", "gp_comm_set_tuning", "gp_comm_set_trace", "gp_comm_set_iteration_source", "gp_comm_set_protocol", "gp_comm_info", "gp_comm_destroy",
     "gp_comm_set_call_counter", "gp_ring_plan",
     "gp_allreduce", "gp_allreduce_ex", "gp_allreduce_emulated", "gp_allreduce_emulated_ex",
     "gp_gather_sum", "gp_broadcast", "gp_gather_sum_emulated", "gp_broadcast_emulated",
@@ -56,6 +56,7 @@ _SIGS = {
     "gp_comm_set_tuning": (_i, [_vp, _i, _d]),
     "gp_comm_set_trace": (_i, [_vp, _vp]),
     "gp_comm_set_iteration_source": (_i, [_vp, _vp]),
+    "gp_comm_set_protocol": (_i, [_vp, ctypes.c_uint64]),
     "gp_comm_info": (_i, [_vp, ctypes.POINTER(ctypes.c_int64)]),
     "gp_comm_set_call_counter": (_i, [_vp, ctypes.c_uint64]),
     "gp_ring_plan": (_i, [_u64, _i, _i, _i, _i, _u64, ctypes.POINTER(ctypes.c_int64)]),

@@ -30,6 +30,44 @@ __global__ void __launch_bounds__(kCT) p2p_copy_kernel(uint4* __restrict__ dst, 
   const uint64_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)kCT + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)kCT) >> 5;
+  if (mode & 8) {
+    // bit 3: CTA-aggregated publish -- every warp copies one chunk, the CTA
+    // meets at a barrier, one thread issues ONE system fence and relaxed
+    // flag stores for all of the CTA's chunks (instead of a release per warp)
+    __shared__ uint64_t s_chunks[kCT / 32];
+    for (;;) {
+      uint64_t c = 0;
+      if (lane == 0) c = atomicAdd(counter, 1ull);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      const uint64_t b0 = c * chunk;
+      if (b0 < nvec) {
+        const uint64_t e0 = min(nvec, b0 + chunk);
+        for (uint64_t base = b0; base < e0; base += 32 * kCU) {
+          uint4 v[kCU];
+#pragma unroll
+          for (int u = 0; u < kCU; ++u) {
+            const uint64_t i = base + u * 32 + lane;
+            if (i < e0) v[u] = pull ? __ldcg(src + i) : __ldg(src + i);
+          }
+#pragma unroll
+          for (int u = 0; u < kCU; ++u) {
+            const uint64_t i = base + u * 32 + lane;
+            if (i < e0) __stcg(dst + i, v[u]);
+          }
+        }
+      }
+      if (lane == 0) s_chunks[threadIdx.x >> 5] = b0 < nvec ? c : ~0ull;
+      const int any = __syncthreads_or(b0 < nvec);
+      if (!any) break;
+      if (threadIdx.x == 0) {
+        fence_sys();
+        for (int w = 0; w < kCT / 32; ++w)
+          if (s_chunks[w] != ~0ull) st_relaxed_sys(flags + s_chunks[w], 1);
+      }
+      __syncthreads();
+    }
+    return;
+  }
   if (mode & 2) {
     for (;;) {
       uint64_t c = 0;
@@ -109,7 +147,7 @@ int gp_calib_p2p_copy_ex(void* dst, const void* src, uint64_t bytes, int ctas, i
     return GP_ERR_ARG;
   }
   if (ctas <= 0) ctas = 148;
-  if ((mode & 2) && (!counter || chunk_bytes < 16 || ((mode & 4) && !flags))) {
+  if ((mode & 10) && (!counter || chunk_bytes < 16 || ((mode & 12) && !flags))) {
     gp_set_error_string("chunked p2p copy needs a counter, chunk size and (mode 4) flags");
     return GP_ERR_ARG;
   }

@@ -185,6 +185,18 @@ __device__ __forceinline__ FV<CodecT<C>::E> decode_v(const uint4& p, float s) {
   return v;
 }
 
+// Partial groups (at most two per block and chunk edge) take out-of-line
+// element-wise paths: inlined at every load / store site they were a large
+// share of the ring kernels' instruction bytes, which small calls fetch cold.
+template <int E, bool NC>
+__device__ __noinline__ FV<E> load_fv_edge(const float* x, uint64_t g0, uint64_t lo, uint64_t hi) {
+  FV<E> r;
+  for (int i = 0; i < E; ++i)
+    r.v[i] = (g0 + i >= lo && g0 + i < hi && GP_ACCESS_OK(x + g0 + i, 4, false))
+                 ? (NC ? __ldg(x + g0 + i) : __ldcg(x + g0 + i)) : 0.f;
+  return r;
+}
+
 // fp32 values x[g0 .. g0+E) restricted to [lo, hi); outside lanes read 0.
 // NC=true uses the read-only path (inputs not written by this launch).
 template <int E, bool NC = true>
@@ -203,10 +215,7 @@ __device__ __forceinline__ FV<E> load_fv(const float* x, uint64_t g0, uint64_t l
       r.v[4 * k] = a.x; r.v[4 * k + 1] = a.y; r.v[4 * k + 2] = a.z; r.v[4 * k + 3] = a.w;
     }
   } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i)
-      r.v[i] = (g0 + i >= lo && g0 + i < hi && GP_ACCESS_OK(x + g0 + i, 4, false))
-                   ? (NC ? __ldg(x + g0 + i) : __ldcg(x + g0 + i)) : 0.f;
+    r = load_fv_edge<E, NC>(x, g0, lo, hi);
   }
   return r;
 }
@@ -264,6 +273,12 @@ __device__ __forceinline__ FV<E> load_fv_pol(const float* x, uint64_t g0, uint64
 }
 
 template <int E>
+__device__ __noinline__ void store_fv_edge(float* x, uint64_t g0, uint64_t lo, uint64_t hi, const FV<E> r) {
+  for (int i = 0; i < E; ++i)
+    if (g0 + i >= lo && g0 + i < hi && GP_ACCESS_OK(x + g0 + i, 4, true)) x[g0 + i] = r.v[i];
+}
+
+template <int E>
 __device__ __forceinline__ void store_fv(float* x, uint64_t g0, uint64_t lo, uint64_t hi, const FV<E>& r) {
   if (lo <= g0 && g0 + E <= hi) {
     float4* p = reinterpret_cast<float4*>(x + g0);
@@ -271,20 +286,15 @@ __device__ __forceinline__ void store_fv(float* x, uint64_t g0, uint64_t lo, uin
 #pragma unroll
     for (int k = 0; k < E / 4; ++k) p[k] = make_float4(r.v[4 * k], r.v[4 * k + 1], r.v[4 * k + 2], r.v[4 * k + 3]);
   } else {
-#pragma unroll
-    for (int i = 0; i < E; ++i)
-      if (g0 + i >= lo && g0 + i < hi && GP_ACCESS_OK(x + g0 + i, 4, true)) x[g0 + i] = r.v[i];
+    store_fv_edge<E>(x, g0, lo, hi, r);
   }
 }
 
 // Payload vector of the group whose first element is `rel0` elements past
 // the slot origin; only elements [vlo, vhi) of the group exist.
 template <int C>
-__device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, int vlo, int vhi) {
-  constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
-  const uint8_t* base = slot + rel0 * W;
-  if (!GP_ACCESS_OK(base + vlo * W, (vhi - vlo) * W, false)) return make_uint4(0, 0, 0, 0);
-  if (vlo == 0 && vhi == E) return __ldcg(reinterpret_cast<const uint4*>(base));
+__device__ __noinline__ uint4 load_pay_edge(const uint8_t* base, int vlo, int vhi) {
+  constexpr int W = CodecT<C>::W;
   uint32_t w[4] = {0, 0, 0, 0};
   for (int i = vlo; i < vhi; ++i) {
     uint32_t e;
@@ -298,11 +308,32 @@ __device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, in
 }
 
 template <int C>
+__device__ __forceinline__ uint4 load_pay(const uint8_t* slot, uint64_t rel0, int vlo, int vhi) {
+  constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
+  const uint8_t* base = slot + rel0 * W;
+  if (!GP_ACCESS_OK(base + vlo * W, (vhi - vlo) * W, false)) return make_uint4(0, 0, 0, 0);
+  if (vlo == 0 && vhi == E) return __ldcg(reinterpret_cast<const uint4*>(base));
+  return load_pay_edge<C>(base, vlo, vhi);
+}
+
+template <int C>
 __device__ __forceinline__ uint4 load_pay_pol(const uint8_t* slot, uint64_t rel0, int vlo, int vhi, uint64_t pol) {
   constexpr int E = CodecT<C>::E, W = CodecT<C>::W;
   if (vlo == 0 && vhi == E && GP_ACCESS_OK(slot + rel0 * W, 16, false))
     return ldcg_hint(reinterpret_cast<const uint4*>(slot + rel0 * W), pol);
   return load_pay<C>(slot, rel0, vlo, vhi);
+}
+
+template <int C>
+__device__ __noinline__ void store_pay_edge(uint8_t* base, int vlo, int vhi, const uint4 p) {
+  constexpr int W = CodecT<C>::W;
+  for (int i = vlo; i < vhi; ++i) {
+    const uint32_t word = wget(p, (i * W) >> 2);
+    const int bit = (i * W * 8) & 31;
+    if constexpr (W == 4) reinterpret_cast<uint32_t*>(base)[i] = word;
+    else if constexpr (W == 2) reinterpret_cast<uint16_t*>(base)[i] = (uint16_t)(word >> bit);
+    else base[i] = (uint8_t)(word >> bit);
+  }
 }
 
 template <int C>
@@ -314,13 +345,7 @@ __device__ __forceinline__ void store_pay(uint8_t* slot, uint64_t rel0, int vlo,
     __stcg(reinterpret_cast<uint4*>(base), p);
     return;
   }
-  for (int i = vlo; i < vhi; ++i) {
-    const uint32_t word = wget(p, (i * W) >> 2);
-    const int bit = (i * W * 8) & 31;
-    if constexpr (W == 4) reinterpret_cast<uint32_t*>(base)[i] = word;
-    else if constexpr (W == 2) reinterpret_cast<uint16_t*>(base)[i] = (uint16_t)(word >> bit);
-    else base[i] = (uint8_t)(word >> bit);
-  }
+  store_pay_edge<C>(base, vlo, vhi, p);
 }
 
 template <int E>

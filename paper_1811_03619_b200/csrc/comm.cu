@@ -83,6 +83,7 @@ struct gp_comm {
   unsigned long long* trace = nullptr;  // optional device timeline buffer
   const uint32_t* iteration_dev = nullptr;  // optional device-resident iteration tag
   uint64_t bar_gen = 0;                 // gp_comm_barrier generations issued
+  uint64_t ll_max = ~0ull;              // gp_comm_set_protocol: largest LL block payload (bytes)
 };
 
 namespace {
@@ -351,6 +352,12 @@ int gp_comm_set_tuning(gp_comm* c, int ctas, double timeout_s) {
   return GP_OK;
 }
 
+int gp_comm_set_protocol(gp_comm* c, uint64_t ll_max_bytes) {
+  if (!c) return fail(GP_ERR_ARG, "null communicator");
+  c->ll_max = ll_max_bytes;
+  return GP_OK;
+}
+
 int gp_comm_set_iteration_source(gp_comm* c, const uint32_t* device_tag) {
   if (!c) return fail(GP_ERR_ARG, "null communicator");
   if (device_tag && (reinterpret_cast<uintptr_t>(device_tag) & 3u)) return fail(GP_ERR_ARG, "misaligned tag");
@@ -492,7 +499,7 @@ static int launch(gp_comm* c, const float* const* ins, float* const* outs, void*
   P.iteration = iteration;
   P.iteration_dev = c->iteration_dev;
   {
-    const RingPlan pl = plan_ring(n, p, c->G, codec, P.pre, c->L.ll_cap);
+    const RingPlan pl = plan_ring(n, p, c->G, codec, P.pre, std::min(c->L.ll_cap, c->ll_max));
     P.chunk = pl.chunk;
     P.G = pl.ctas;
     P.ll = pl.ll;

@@ -74,8 +74,8 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // causes (header mismatch, own timeout, non-finite); a wait that only ended
 // because a peer aborted (timeout kind, detail 1) is reported only when the
 // rank has no cause of its own. Steps fit 7 bits (p <= 8).
-__device__ __forceinline__ void latch_error(ErrWord* e, int kind, int phase, int step, int block,
-                                            int rank, int detail) {
+inline __device__ __noinline__ void latch_error(ErrWord* e, int kind, int phase, int step, int block,
+                                         int rank, int detail) {
   const unsigned long long consequence = (kind == kErrTimeout && detail == 1) ? 1ull : 0ull;
   const unsigned long long code =
       (consequence << 63) | ((unsigned long long)(phase_order(phase) & 0x7) << 60) |

@@ -249,7 +249,11 @@ __device__ __forceinline__ void warp_publish(const RingParams& P, uint8_t* dst, 
   __syncwarp();
   if (lane_id() == 0) {
     if (c == 0) write_hdr(P, dst, slot, block, len, scale);
+#ifdef PIPESGD_EXP_NOFENCE  // timing experiment only (no ordering: results may be wrong)
+    st_relaxed_sys(flag_ptr(dst, P.L, slot, c), flag_word(scale));
+#else
     st_release_sys(flag_ptr(dst, P.L, slot, c), flag_word(scale));  // release: orders the warp's stores
+#endif
   }
 }
 
@@ -260,7 +264,9 @@ __device__ __forceinline__ void warp_publish_all(const RingParams& P, const Rank
   if (lane_id() == 0) {
     if (c == 0)
       for (int d = 1; d < P.p; ++d) write_hdr(P, R.peer[(R.rank + d) % P.p], ag_slot(P.p, b), b, len, scale);
+#ifndef PIPESGD_EXP_NOFENCE
     fence_sys();  // one system fence, then relaxed flag stores to every peer
+#endif
     for (int d = 1; d < P.p; ++d)
       st_relaxed_sys(flag_ptr(R.peer[(R.rank + d) % P.p], P.L, ag_slot(P.p, b), c), flag_word(scale));
   }
@@ -347,13 +353,19 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
 #ifndef PIPESGD_Q8_UNROLL
 #define PIPESGD_Q8_UNROLL 1
 #endif
-template <int C, typename L, typename S>
+#ifndef PIPESGD_LL_UNROLL
+#define PIPESGD_LL_UNROLL 1
+#endif
+template <int C, bool LLM = false, typename L, typename S>
 __device__ __forceinline__ void for_groups(const RingParams& P, const Blk& B, uint32_t c, L&& load, S&& use) {
   constexpr int E = CodecT<C>::E;
   // groups per lane per batch: 1024-element batches, except quant8 whose
   // 16-element groups and encode temporaries would spill at the 128-register
-  // budget with two in flight
-  constexpr int U = C == kQuant8 ? PIPESGD_Q8_UNROLL : (int)kBatch / (32 * E);
+  // budget with two in flight, and the LL protocol: its chunks are 128
+  // elements (one group per lane), and every unrolled copy of an LL poll +
+  // encode + line store is instruction bytes a latency-bound call fetches
+  // cold (the none kernel was 246 KB of SASS)
+  constexpr int U = C == kQuant8 ? PIPESGD_Q8_UNROLL : LLM ? PIPESGD_LL_UNROLL : (int)kBatch / (32 * E);
   constexpr uint64_t kB = 32ull * E * U;
   const int lane = lane_id();
   const uint64_t cbase = B.A + (uint64_t)c * P.chunk;
@@ -468,7 +480,7 @@ __device__ __noinline__ bool ring_access_ok(const void* ptr, uint64_t bytes, boo
 }
 #endif
 
-template <int C, bool LL>
+template <int C, bool LL, bool PRE>
 __device__ __forceinline__ void ring_body(const RingParams& P) {
   constexpr int E = CodecT<C>::E;
   const int G = P.G;
@@ -502,7 +514,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   // its scale needs max|grad| over the whole vector: one extra read pass.
   Q8 q0 = q8_make(0.f);
   auto px = [&](FV<E> v) -> FV<E> {
-    if (P.pre) {
+    if constexpr (PRE) {
       if constexpr (C != kQuant8) {  // quant8: the whole-vector max pass already checked every x
 #pragma unroll
         for (int i = 0; i < E; ++i) bad |= nonfinite(v.v[i]);
@@ -598,7 +610,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       const int o = (b - 1 + p) % p;
       uint8_t* dst = slot_ptr(R.peer[o], P.L, rs_slot(d));
       uint8_t* lld = ll_ptr(R.peer[o], P.L, rs_slot(d));
-      for_groups<C>(P, B, c,
+      for_groups<C, LL>(P, B, c,
                     [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
                       const uint4 pk = encode_v<C>(px(v), q, bad);
@@ -705,11 +717,11 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       Q8 q = q8_make(0.f);
       if constexpr (C == kQuant8) {
         float vmax;
-        if (!P.pre) {
+        if constexpr (!PRE) {
           uint32_t m = 0;
           const uint64_t keep = l2_evict_last();  // the send pass below re-reads the block
           for (uint32_t c = wid; c < B.nch; c = grab(ctl, 0, NW))
-            for_groups<C>(P, B, c,
+            for_groups<C, LL>(P, B, c,
                           [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
                             return load_fv_pol<E>(x, g0, lo, hi, keep);
                           },
@@ -725,7 +737,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           W.nch = P.n ? (uint32_t)((P.n + P.chunk - 1) / P.chunk) : 0u;
           uint32_t m = 0, mo = 0;
           for (uint32_t c = wid; c < W.nch; c = grab(ctl, 0, NW))
-            for_groups<C>(P, W, c,
+            for_groups<C, LL>(P, W, c,
                           [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                           [&](uint64_t g0, uint64_t, uint64_t, int, int, const FV<E>& v) {
                             m = max(m, absmax_bits(v));
@@ -753,7 +765,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       uint8_t* lld = ll_ptr(R.peer[succ], P.L, rs_slot(0));
       bool first0 = true;
       for (uint32_t c = wid; c < B.nch; c = grab(ctl, 1, NW)) {
-        for_groups<C>(P, B, c,
+        for_groups<C, LL>(P, B, c,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                       [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
                         // quant8: finiteness is known from the block max
@@ -827,7 +839,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
             return;
           }
           if (first) stamp(P, wid, lr, tr_step(s, 0));
-          for_groups<C>(P, B, c, load_xin,
+          for_groups<C, LL>(P, B, c, load_xin,
                         [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi, const XIn<E>& v) {
                           emit(g0, lo, hi, vlo, vhi, encode_v<C>(add_v(px(v.x), decode_v<C>(v.in, sin)), q, bad),
                                0.f);
@@ -866,7 +878,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           }
           if (first) stamp(P, wid, lr, tr_step(s, 0));
           first = false;
-          for_groups<C>(P, B, c,
+          for_groups<C, LL>(P, B, c,
                         [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
                           return load_xin_pol(g0, lo, hi, vlo, vhi, keep);
                         },
@@ -892,7 +904,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           } else if (!warp_await(P, R, ctl, err, rs_slot(s), c, kPhRS, s, b, B.len, sin)) {
             return;
           }
-          for_groups<C>(P, B, c,
+          for_groups<C, LL>(P, B, c,
                         [&](uint64_t g0, uint64_t lo, uint64_t hi, int vlo, int vhi) {
                           return load_xin_pol(g0, lo, hi, vlo, vhi, drop);
                         },
@@ -971,7 +983,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       }
       if (k == 1 && first) stamp(P, wid, lr, kTrAgIn);
       first = false;
-      for_groups<C>(P, B, c,
+      for_groups<C, LL>(P, B, c,
                     [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi) {
                       return ll ? ll_load(ll_in, g0 - B.A) : load_pay<C>(in_slot, g0 - B.A, vlo, vhi);
                     },
@@ -993,7 +1005,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
 #ifndef PIPESGD_RING_MINBLOCKS
 #define PIPESGD_RING_MINBLOCKS (2048 / kRingThreads / 4 > 0 ? 2048 / kRingThreads / 4 : 1)
 #endif
-template <int C, bool LL>
+// PRE (the fused local pre-compress) is a template parameter like the codec
+// and the protocol: each kernel carries only the code its calls execute, and
+// a small call fetches that code cold (see for_groups).
+template <int C, bool LL, bool PRE>
 __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     ring_allreduce_kernel(const __grid_constant__ RingParams P) {
   const int lr = blockIdx.x / P.G;
@@ -1022,7 +1037,7 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
     }
   }
   __syncthreads();
-  ring_body<C, LL>(P);  // returns early (per warp) on timeout / abort / header mismatch
+  ring_body<C, LL, PRE>(P);  // returns early (per warp) on timeout / abort / header mismatch
   // The last warp of this rank to leave closes the call by advancing the call
   // count. The next call on this stream starts only after this kernel has
   // completed, which also makes the bank zeroing above visible to it.
@@ -1033,17 +1048,17 @@ __global__ void __launch_bounds__(kRingThreads, PIPESGD_RING_MINBLOCKS)
   }
 }
 
+// every ring kernel instantiation, indexed [codec][ll][pre]
+#define GP_RING_FNS(C) \
+  {{(const void*)ring_allreduce_kernel<C, false, false>, (const void*)ring_allreduce_kernel<C, false, true>}, \
+   {(const void*)ring_allreduce_kernel<C, true, false>, (const void*)ring_allreduce_kernel<C, true, true>}}
+static const void* const kRingFns[3][2][2] = {GP_RING_FNS(kNone), GP_RING_FNS(kTrunc16), GP_RING_FNS(kQuant8)};
+#undef GP_RING_FNS
+
 void launch_ring(const RingParams& P, int nlocal, cudaStream_t stream, cudaError_t* err) {
   void* args[] = {const_cast<RingParams*>(&P)};
   const dim3 grid(P.G * nlocal), block(kRingThreads);
-  const void* fn = P.codec == kNone
-                       ? (P.ll ? (const void*)ring_allreduce_kernel<kNone, true>
-                               : (const void*)ring_allreduce_kernel<kNone, false>)
-                   : P.codec == kTrunc16
-                       ? (P.ll ? (const void*)ring_allreduce_kernel<kTrunc16, true>
-                               : (const void*)ring_allreduce_kernel<kTrunc16, false>)
-                       : (P.ll ? (const void*)ring_allreduce_kernel<kQuant8, true>
-                               : (const void*)ring_allreduce_kernel<kQuant8, false>);
+  const void* fn = kRingFns[P.codec][P.ll ? 1 : 0][P.pre ? 1 : 0];
   // Emulated rings (nlocal > 1) need every CTA co-resident: cooperative
   // launch. A single rank per GPU only needs its G <= #SM CTAs to become
   // resident eventually (no CTA waits on a CTA of its own launch except the
@@ -1064,17 +1079,13 @@ int ring_warps_per_cta() { return kWarps; }
 
 int ring_max_ctas_per_sm() {
   int m = 1 << 30;
-  const void* fns[6] = {(const void*)ring_allreduce_kernel<kNone, false>,
-                        (const void*)ring_allreduce_kernel<kTrunc16, false>,
-                        (const void*)ring_allreduce_kernel<kQuant8, false>,
-                        (const void*)ring_allreduce_kernel<kNone, true>,
-                        (const void*)ring_allreduce_kernel<kTrunc16, true>,
-                        (const void*)ring_allreduce_kernel<kQuant8, true>};
-  for (const void* f : fns) {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, kRingThreads, 0);
-    m = std::min(m, std::max(b, 1));
-  }
+  for (const auto& per_codec : kRingFns)
+    for (const auto& per_ll : per_codec)
+      for (const void* f : per_ll) {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, kRingThreads, 0);
+        m = std::min(m, std::max(b, 1));
+      }
   return m;
 }
 

@@ -24,12 +24,15 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 // itself and no release fence / flag store is needed, at twice the bytes.
 // A call of any codec takes it (quant8's block scale rides in the header
 // line's fourth word) when its block payload (elements incl. the
-// 16-element alignment slack x wire width) is at most kLLHopBytes x (p - 1):
-// every further hop saves one more fence (measured crossover: 512 KB at
-// p = 2, >= 1 MB at p = 4; profiles/r01_c5/ll_threshold_ab.log). Compile-time
-// constants, so every rank makes the same choice.
+// 16-element alignment slack x wire width) fits the 2 MiB LL slot. Measured
+// (profiles/r02/ll_region_ab/, after the LL path's code shrank to one group
+// per lane): 2 MiB blocks beat the flag protocol at p = 2 (codec none at
+// C1's 2.6 MB 34 -> 25 us, trunc16 at 4 MiB 26 -> 19 us, quant8 at 8 MiB
+// 43 -> 35 us) and at p = 4 (none at 6 MiB 70 -> 57 us, trunc16 at 12 MiB
+// 67 -> 57 us); a 4 MiB slot lost at p = 4 (none at 12 MiB 79 -> 105 us).
+// Compile-time constants, so every rank makes the same choice.
 #ifndef PIPESGD_LL_HOP_BYTES
-#define PIPESGD_LL_HOP_BYTES (512u << 10)
+#define PIPESGD_LL_HOP_BYTES (1u << 20)
 #endif
 #ifndef PIPESGD_LL_REGION_BYTES
 #define PIPESGD_LL_REGION_BYTES (2u << 20)
@@ -37,10 +40,8 @@ constexpr uint32_t kMaxChunk = 16384;  // default largest warp chunk (64 KiB of 
 constexpr uint64_t kLLHopBytes = PIPESGD_LL_HOP_BYTES;
 constexpr uint64_t kLLRegionBytes = PIPESGD_LL_REGION_BYTES;  // largest LL block payload (fixed: layouts agree)
 
-// p = 2 takes LL up to 1 MiB blocks (with the short LL chunks, trunc16 at
-// C1's size 27 -> 16 us, quant8 at 4 MiB 40 -> 32 us); from p = 3 on, LL
-// above 512 KiB x (p - 1) lost to the flag protocol (none at 8 MiB, p = 4:
-// 71 -> 79 us). profiles/r02/ll_threshold_ab/.
+// hop budget x (p - 1), twice it at p = 2, capped by the slot: 2 MiB for
+// every p at the defaults
 __host__ __device__ inline uint64_t ll_payload_limit(int p) {
   const uint64_t v = p == 2 ? 2 * kLLHopBytes : kLLHopBytes * (uint64_t)(p > 1 ? p - 1 : 1);
   return v < kLLRegionBytes ? v : kLLRegionBytes;
@@ -97,7 +98,8 @@ __device__ __forceinline__ int abort_detail(const Ctl* ctl, int rank) {
 }
 
 // Poison this communicator on every rank (peers' ctl blocks over NVLink).
-__device__ __forceinline__ void abort_all(uint8_t* const* peer, int p, uint64_t off_ctl, uint32_t seq, int rank) {
+// Out of line: an error path, reached from every wait site.
+inline __device__ __noinline__ void abort_all(uint8_t* const* peer, int p, uint64_t off_ctl, uint32_t seq, int rank) {
   const unsigned long long w = kAbortSticky | ((unsigned long long)((rank + 1) & 0xFF) << 32) | seq;
   for (int q = 0; q < p; ++q) {
     Ctl* c = reinterpret_cast<Ctl*>(peer[q] + off_ctl);

@@ -331,8 +331,20 @@ def barrier_time(endpoint, rounds: int = 200) -> float:
     return t / 1e9 / rounds
 
 
+def ring_fixed_overhead(measured_small_s: float, p: int, n_small: int, alpha: float, beta: float, gamma: float,
+                        sync: float) -> float:
+    """The per-call cost Eq. 5 has no term for -- kernel launch, call open /
+    close, the first chunk's ramp -- calibrated as Eq. 5's residual on the
+    smallest real call (n_small = 16 elements per rank, codec none), >= 0.
+    Used only by the extended model (compare_ring eq5_ext), on every larger
+    size, so no row predicts itself."""
+    params = ClusterParams(workers=p, latency_s=alpha, byte_time_s=beta, reduce_time_s=gamma, sync_time_s=sync,
+                           model_bytes=float(4 * n_small))
+    return max(0.0, measured_small_s - ring_comm_time(params))
+
+
 def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: float, gamma: float, sync: float,
-                 delta: float = 0.0, flag_threshold: float = 0.25) -> dict:
+                 delta: float = 0.0, flag_threshold: float = 0.25, fixed_s: float = 0.0) -> dict:
     """One prediction-vs-measurement row for a ring call (compare_prediction,
     harness.py:687-720, applied to Eq. 5 itself): n is the element count,
     model bytes are the codec's payload (harness.py:562).
@@ -343,8 +355,8 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
     the allgather's decode of the p-1 received blocks into the fp32 output,
     (p-1)/p n delta (delta = decode time per element). For none / trunc16 the
     step-0 encode streams straight onto the link and the decode overlaps the
-    owners' pushes, so eq5_ext == Eq. 5 (measured: 0.93-1.14 of the ring at
-    >= 64 MiB, profiles/r02/c5)."""
+    owners' pushes. Every codec's eq5_ext also adds `fixed_s`, the per-call
+    cost calibrated on the smallest call (ring_fixed_overhead)."""
     from .compression import as_codec
 
     nb = float(n * as_codec(codec).bytes_per_elem)
@@ -355,12 +367,13 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
     q8 = as_codec(codec).name.lower() == "quant8"
     step0 = nb / p * gamma if (p > 1 and q8) else 0.0
     ag = (p - 1) / p * n * delta if q8 else 0.0
-    ext = pred + step0 + ag
+    ext = pred + step0 + ag + fixed_s
     rel = (measured_s - pred) / pred if pred > 0 else float("inf")
     rel_ext = (measured_s - ext) / ext if ext > 0 else float("inf")
     return {"n": n, "codec": as_codec(codec).name.lower(), "measured_ms": measured_s * 1e3, "eq5_ms": pred * 1e3,
             "terms_us": {"latency": lat * 1e6, "bandwidth": bw * 1e6, "reduction": red * 1e6, "sync": syn * 1e6,
-                         "ext_step0_encode": step0 * 1e6, "ext_allgather_decode": ag * 1e6},
+                         "ext_step0_encode": step0 * 1e6, "ext_allgather_decode": ag * 1e6,
+                         "ext_fixed_per_call": fixed_s * 1e6},
             "eq5_over_measured": pred / measured_s if measured_s > 0 else None, "rel_error": rel,
             "flagged": abs(rel) > flag_threshold,
             "eq5_ext_ms": ext * 1e3, "eq5_ext_over_measured": ext / measured_s if measured_s > 0 else None,

@@ -182,6 +182,16 @@ def raise_for(e, p: int, n: int, timeout_s: float) -> Exception:
     return CollectiveError(f"{phase} step {e.step}: device error kind {e.kind}")
 
 
+def _set_protocol(comm, ll_max_bytes: int | None) -> None:
+    """ll_max_bytes (every rank the same): LL protocol only for blocks whose
+    payload fits it, 0 = flag protocol always; None = the library default
+    (LL up to 2 MiB blocks). Results are bit-identical either way."""
+    if ll_max_bytes is not None:
+        if ll_max_bytes < 0:
+            raise ConfigError("ll_max_bytes must be >= 0")
+        _lib.call("gp_comm_set_protocol", comm, int(ll_max_bytes))
+
+
 class GpuTransport:
     """In-process ring over p GPUs (rank r on devices[r]); threads play ranks,
     exactly like the reference's InProcTransport (transport.py:150-177).
@@ -194,7 +204,7 @@ class GpuTransport:
 
     def __init__(self, world_size: int, latency_s: float = 0.0, byte_time_s: float = 0.0,
                  timeout_s: float = DEFAULT_TIMEOUT_S, devices=None, max_elems: int = DEFAULT_MAX_ELEMS,
-                 ctas: int = 0):
+                 ctas: int = 0, ll_max_bytes: int | None = None):
         if world_size < 1:
             raise ConfigError("need at least one rank")
         if latency_s or byte_time_s:
@@ -211,6 +221,7 @@ class GpuTransport:
         self._comms = [_comm_create(r, world_size, devices[r], max_elems) for r in range(world_size)]
         for c in self._comms:
             _lib.call("gp_comm_set_tuning", c, int(ctas), float(timeout_s))
+            _set_protocol(c, ll_max_bytes)
         # chunk size, and so every flag index, follows the CTA budget G: all
         # ranks must agree even when their devices' caps differ
         g = min(ep_ctas(c) for c in self._comms)
@@ -270,7 +281,7 @@ class EmulatedTransport:
 
     def __init__(self, world_size: int, latency_s: float = 0.0, byte_time_s: float = 0.0,
                  timeout_s: float = DEFAULT_TIMEOUT_S, device: int = 0,
-                 max_elems: int = DEFAULT_MAX_ELEMS // 4, ctas: int = 0):
+                 max_elems: int = DEFAULT_MAX_ELEMS // 4, ctas: int = 0, ll_max_bytes: int | None = None):
         if latency_s or byte_time_s:
             raise ConfigError("GPU transports do not inject synthetic delays")
         self.world_size = world_size
@@ -280,6 +291,7 @@ class EmulatedTransport:
         _lib.call("gp_comm_create_emulated", world_size, device, max_elems, ctypes.byref(h))
         self._comm = h
         _lib.call("gp_comm_set_tuning", h, int(ctas), float(timeout_s))
+        _set_protocol(h, ll_max_bytes)
         self._cv = threading.Condition()
         self._cur = _Generation()
         self._poll_lock = threading.Lock()
@@ -413,7 +425,7 @@ class ProcessGroupTransport:
 
     @staticmethod
     def endpoint(device: int | None = None, group=None, timeout_s: float = DEFAULT_TIMEOUT_S,
-                 max_elems: int = DEFAULT_MAX_ELEMS, ctas: int = 0) -> GpuEndpoint:
+                 max_elems: int = DEFAULT_MAX_ELEMS, ctas: int = 0, ll_max_bytes: int | None = None) -> GpuEndpoint:
         import torch.distributed as dist
 
         rank = dist.get_rank(group)
@@ -422,6 +434,7 @@ class ProcessGroupTransport:
             device = torch.cuda.current_device()
         comm = _comm_create(rank, world, device, max_elems)
         _lib.call("gp_comm_set_tuning", comm, int(ctas), float(timeout_s))
+        _set_protocol(comm, ll_max_bytes)
         if world > 1:
             h = ctypes.create_string_buffer(64)
             _lib.call("gp_comm_ipc_handle", comm, h)

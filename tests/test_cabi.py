@@ -96,11 +96,11 @@ def _plan(n, world, ctas, codec, flags=0, max_elems=None):
 
 @pytest.mark.parametrize("world,codec", [(2, 0), (2, 1), (2, 2), (4, 0), (4, 1), (8, 0), (8, 2)])
 def test_ll_protocol_threshold(world, codec):
-    """LL iff the block payload (incl. 16 elements of slack) fits 1 MiB at
-    p = 2 and 512 KiB x (p - 1) from p = 3 on, capped at 2 MiB
+    """LL iff the block payload (incl. 16 elements of slack) fits 2 MiB at
+    p = 2 and 1 MiB x (p - 1) from p = 3 on, capped at the 2 MiB LL slot
     (ring.cuh:ll_payload_limit)."""
     w = (4, 2, 1)[codec]
-    limit = min((1 << 20) if world == 2 else (512 << 10) * (world - 1), 2 << 20)
+    limit = min((2 << 20) if world == 2 else (1 << 20) * (world - 1), 2 << 20)
     n_max = world * (limit // w - 16)  # largest n whose ceil(n/p) + 16 blocks fit
     assert _plan(n_max, world, 592, codec)["ll"] == 1
     assert _plan(n_max + world, world, 592, codec)["ll"] == 0

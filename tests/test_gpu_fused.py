@@ -93,11 +93,11 @@ def test_fused_variants_emulated(P, p):
         tr.close()
 
 
-@pytest.mark.parametrize("n", [4_710_538, 150_001])  # flag protocol / LL protocol
+@pytest.mark.parametrize("n,ll", [(4_710_538, 0), (150_001, None)])  # flag protocol / LL protocol
 @pytest.mark.parametrize("codec", [0, 1, 2])
-def test_fused_variants_p2p(P, codec, n):
+def test_fused_variants_p2p(P, codec, n, ll):
     p = 4  # per-rank launches: one GPU per rank, or ranks sharing GPUs
-    tr = real_transport(P, p, timeout_s=60.0, max_elems=n)
+    tr = real_transport(P, p, timeout_s=60.0, max_elems=n, ll_max_bytes=ll)
     devs = [tr.endpoint(r).device for r in range(p)]
     try:
         ins = inputs(p, n, 77 + codec, scale_exp=-3)

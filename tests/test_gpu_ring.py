@@ -197,8 +197,8 @@ def test_p2p_failure_poisons_every_later_call(P):
 
 
 @multigpu
-@pytest.mark.parametrize("n", [300_007, 50_001])  # flag protocol / LL protocol (none, trunc16)
-def test_p2p_ring_in_cuda_graph_replays_bit_exact(P, n):
+@pytest.mark.parametrize("n,ll", [(300_007, 0), (50_001, None)])  # flag protocol / LL protocol
+def test_p2p_ring_in_cuda_graph_replays_bit_exact(P, n, ll):
     """The call sequence number lives on the device, so one captured launch
     can be replayed as many calls (what graph-captured training steps need)."""
     from paper_1811_03619_b200.collective import allreduce_into
@@ -207,7 +207,7 @@ def test_p2p_ring_in_cuda_graph_replays_bit_exact(P, n):
     g = np.random.default_rng(5)
     ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
     want = {c: OR.ring_allreduce_all(ins, int(c)).outputs[0] for c in P.Codec}
-    tr = real_transport(P, p, timeout_s=30.0, max_elems=n)
+    tr = real_transport(P, p, timeout_s=30.0, max_elems=n, ll_max_bytes=ll)
 
     def op(r, ep):
         dev = ep.device
@@ -241,11 +241,11 @@ def test_p2p_ring_in_cuda_graph_replays_bit_exact(P, n):
 
 
 @multigpu
-@pytest.mark.parametrize("n", [8, 300_007])  # LL protocol / flag protocol
-def test_p2p_iteration_tag_mismatch_is_a_header_error(P, n):
+@pytest.mark.parametrize("n,ll", [(8, None), (300_007, 0)])  # LL protocol / flag protocol
+def test_p2p_iteration_tag_mismatch_is_a_header_error(P, n, ll):
     """collective.py:52-64: a block carrying another iteration tag is rejected
     (both wire protocols validate the slot header with chunk 0)."""
-    tr = real_transport(P, 2, timeout_s=5.0, max_elems=n)
+    tr = real_transport(P, 2, timeout_s=5.0, max_elems=n, ll_max_bytes=ll)
     try:
         xs = [torch.ones(n, device=tr.endpoint(r).device) for r in range(2)]
         with pytest.raises(P.CollectiveError, match="iteration tag"):
@@ -257,12 +257,12 @@ def test_p2p_iteration_tag_mismatch_is_a_header_error(P, n):
 @multigpu
 def test_p2p_ll_threshold_and_protocol_switching(P):
     """Sizes either side of the LL threshold (at p = 2, blocks whose payload
-    incl. 16 elements of slack is <= 1 MiB use the sequence-tagged LL slots,
+    incl. 16 elements of slack is <= 2 MiB use the sequence-tagged LL slots,
     larger ones the flag protocol), called alternately on one communicator:
     every result equals the reference's, so neither protocol ever reads the
     other's stale bytes."""
     p = 2
-    t = 2 * ((1 << 20) // 4 - 16)  # fp32 threshold; trunc16's is twice that, quant8's 4x
+    t = 2 * ((2 << 20) // 4 - 16)  # fp32 threshold; trunc16's is twice that, quant8's 4x
     sizes = [8, t - 1, t, t + 1, t + 33, 2 * t, 2 * t + 2, 4 * t + 2, 1_000_003, 8, t, 5]
     tr = real_transport(P, p, timeout_s=30.0, max_elems=max(sizes))
     try:
@@ -286,7 +286,7 @@ def test_p2p_ring_across_call_sequence_wrap(P):
     variants included via the graph test's allreduce_into path) stay exact."""
     from paper_1811_03619_b200 import _lib
     p = 2
-    tr = real_transport(P, p, timeout_s=30.0, max_elems=300_007)
+    tr = real_transport(P, p, timeout_s=30.0, max_elems=300_007, ll_max_bytes=256 << 10)
     try:
         for r in range(p):
             _lib.call("gp_comm_set_call_counter", tr.endpoint(r)._comm, 0xFFFFFFFF - 4)
@@ -345,8 +345,8 @@ def test_call_over_capacity_is_a_config_error(P):
 
 
 @multigpu
-@pytest.mark.parametrize("n", [300_007, 50_001])  # flag protocol / LL protocol
-def test_graph_replayed_ring_checks_the_device_iteration_tag(P, n):
+@pytest.mark.parametrize("n,ll", [(300_007, 0), (50_001, None)])  # flag protocol / LL protocol
+def test_graph_replayed_ring_checks_the_device_iteration_tag(P, n, ll):
     """A ring captured once in a CUDA graph reads its iteration tag from
     device memory (gp_comm_set_iteration_source), so the reference's _expect
     check (collective.py:52-64) stays live under replay: equal tags replay
@@ -358,7 +358,7 @@ def test_graph_replayed_ring_checks_the_device_iteration_tag(P, n):
     g = np.random.default_rng(11)
     ins = [g.normal(0, 1, n).astype(np.float32) for _ in range(p)]
     want = OR.ring_allreduce_all(ins, int(P.Codec.TRUNC16)).outputs[0]
-    tr = real_transport(P, p, timeout_s=5.0, max_elems=n)
+    tr = real_transport(P, p, timeout_s=5.0, max_elems=n, ll_max_bytes=ll)
     tags = [[7, 7], [8, 8], [9, 10]]  # the third replay: rank 1 is one iteration ahead
 
     def op(r, ep):

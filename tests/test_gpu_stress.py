@@ -29,7 +29,8 @@ def test_async_call_storm_is_exact(P, p, seed):
         fused = bool(g.integers(0, 4) == 0)
         calls.append((n, codec, fused))
     nmax = max(n for n, _, _ in calls)
-    tr = real_transport(P, p, timeout_s=60.0, max_elems=nmax)
+    # blocks above 256 KiB take the flag protocol: both protocols interleave
+    tr = real_transport(P, p, timeout_s=60.0, max_elems=nmax, ll_max_bytes=256 << 10)
     sample = set(range(0, len(calls), 17))
     base = [g.normal(0, 1, nmax).astype(np.float32) for _ in range(p)]
 

@@ -105,3 +105,21 @@ def test_compare_ring_eq5_terms_and_quant8_extension():
         ext = eq5 + ((nb / p * g + (p - 1) / p * n * d) if codec == "quant8" else 0.0)
         assert abs(row["eq5_ext_ms"] - ext * 1e3) < 1e-12
         assert T.compare_ring(eq5 * 1.3, p, codec, n, a, b, g, S, d)["flagged"]
+
+
+def test_ring_fixed_overhead_is_eq5_residual_on_the_smallest_call():
+    """timing.ring_fixed_overhead: measured smallest call minus its Eq. 5
+    prediction (never negative); compare_ring's eq5_ext adds it to every
+    codec's prediction, the paper's Eq. 5 column is unchanged."""
+    from paper_1811_03619_b200 import timing as T
+    p, a, b, g, S = 4, 2e-6, 1 / 700e9, 1 / 400e9, 5e-6
+    small = 64
+    eq5_small = 2 * (p - 1) * a + 2 * (p - 1) / p * 4 * small * b + (p - 1) / p * 4 * small * g + S
+    fixed = T.ring_fixed_overhead(eq5_small + 7e-6, p, small, a, b, g, S)
+    assert fixed == pytest.approx(7e-6, rel=1e-9)
+    assert T.ring_fixed_overhead(eq5_small / 2, p, small, a, b, g, S) == 0.0
+    row0 = T.compare_ring(30e-6, p, "trunc16", 650_000, a, b, g, S)
+    row = T.compare_ring(30e-6, p, "trunc16", 650_000, a, b, g, S, fixed_s=fixed)
+    assert row["eq5_ms"] == row0["eq5_ms"]
+    assert row["eq5_ext_ms"] == pytest.approx(row0["eq5_ext_ms"] + 7e-3, rel=1e-9)
+    assert row["terms_us"]["ext_fixed_per_call"] == pytest.approx(7.0)

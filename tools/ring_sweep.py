@@ -134,6 +134,17 @@ def main():
         else:
             store.wait(["sweep_eq5_calib"])
         sym = {"S_s": S, **ab}
+        # per-call fixed cost: Eq. 5's residual on the smallest real call
+        # (16 elements per rank, codec none), used by eq5_ext at every size
+        xs = torch.randn(16 * p, device="cuda")
+        ys = torch.empty_like(xs)
+        t_small = timed(lambda: allreduce_into(xs, ys, ep, Codec.NONE, 0, stream), 50, 5, stream)
+        endpoint_wait(ep, 16 * p, stream)
+        if rank == 0 and "alpha_s" in sym:
+            g_small = T.gamma_hop(Codec.NONE, 16, torch.device("cuda", local), ring_ctas=ep.info()["ctas"])
+            sym["fixed_s"] = T.ring_fixed_overhead(t_small, p, 16 * p, sym["alpha_s"], sym["beta_s_per_byte"],
+                                                   g_small, S)
+            sym["small_call_s"] = t_small
         if rank == 0:
             print(json.dumps({"eq5_symbols": sym, "cpu": cpu_name(), "cpu_count": os.cpu_count()}), flush=True)
     for n in sizes:
@@ -171,7 +182,7 @@ def main():
                 gam = T.gamma_hop(codec, max(1, n // p), dv, ring_ctas=ep.info()["ctas"])
                 dlt = T.delta_decode(codec, max(1, n // p), dv)
                 rec["eq5"] = T.compare_ring(t, p, codec, n, sym["alpha_s"], sym["beta_s_per_byte"], gam, sym["S_s"],
-                                            dlt)
+                                            dlt, fixed_s=sym.get("fixed_s", 0.0))
                 rec["eq5"]["gamma_gbs"] = 1 / gam / 1e9 if gam > 0 else None
             if args.cpu_ref_max and n <= args.cpu_ref_max:
                 dist.barrier()
