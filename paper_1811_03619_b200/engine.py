@@ -215,9 +215,11 @@ class RankEngine:
         self.dev = fm.params.device
         self.n = fm.num_params
         self.cs = torch.cuda.Stream(self.dev)
-        # comm stream priority (PIPESGD_COMM_PRIORITY, lower = higher; 0 = same
-        # as compute): its CTAs are scheduled ahead of compute CTAs as SMs free up
-        self.ms = torch.cuda.Stream(self.dev, priority=int(os.environ.get("PIPESGD_COMM_PRIORITY", "0")))
+        # comm stream priority (COMM_PRIORITY; PIPESGD_COMM_PRIORITY overrides;
+        # lower = higher, 0 = same as compute): its CTAs are scheduled ahead of
+        # compute CTAs as SMs free up
+        prio = int(os.environ.get("PIPESGD_COMM_PRIORITY", COMM_PRIORITY))
+        self.ms = torch.cuda.Stream(self.dev, priority=prio)
         # comm_sms > 0: the comm stream lives in a green context of that many
         # SMs (greenctx.py), so the pipelined ring occupies a fixed slice of
         # the GPU; the communicator's CTA budget must fit it (4 CTAs per SM)
@@ -225,7 +227,7 @@ class RankEngine:
         if comm_sms > 0:
             from .greenctx import green_stream
             try:
-                self.ms, self.comm_sms = green_stream(self.dev.index, comm_sms)
+                self.ms, self.comm_sms = green_stream(self.dev.index, comm_sms, prio)
             except Exception as err:  # noqa: BLE001 - no green contexts: plain stream, full budget
                 import warnings
                 warnings.warn(f"green context unavailable ({err}); the comm stream shares every SM")
@@ -763,6 +765,11 @@ class RankEngine:
 #     pipeline). One rank (no ring): C3 58.1 either way, no partition.
 # profiles/r02/engine_ctas/, profiles/r02/green_ctx/.
 COMM_CTAS = 0
+# The comm stream runs at the highest priority (CUDA clamps -5 to the
+# device's range): C3 at N = 1, the pipe re-compress's absmax + encode reach
+# 0.54 of HBM beside cuDNN instead of 0.45, iterations/s unchanged
+# (58.2 / 58.3; profiles/r02/comm_priority/).
+COMM_PRIORITY = -5
 PIPE_SMALL_GRADIENT_CTAS = 64
 PIPE_MID_GRADIENT_SMS = 32
 PIPE_LARGE_GRADIENT_SMS = 48

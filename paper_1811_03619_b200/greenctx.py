@@ -23,7 +23,7 @@ _CONTEXTS: dict = {}
 _LOCK = threading.Lock()
 
 
-def green_stream(device_index: int, sms: int):
+def green_stream(device_index: int, sms: int, priority: int = 0):
     """A new torch ExternalStream bound to a green context of `sms` SMs (the
     driver may round up to its SM granularity). Returns (stream, sm_count).
     The green context is made once per (device, SM count) and shared; every
@@ -36,7 +36,9 @@ def green_stream(device_index: int, sms: int):
         if key not in _CONTEXTS:
             _CONTEXTS[key] = _make_green_ctx(*key)
         gctx, count = _CONTEXTS[key]
-    st = _check(d.cuGreenCtxStreamCreate(gctx, d.CUstream_flags.CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate")
+    # out-of-range priorities are clamped by the driver, as for cuStreamCreateWithPriority
+    st = _check(d.cuGreenCtxStreamCreate(gctx, d.CUstream_flags.CU_STREAM_NON_BLOCKING, int(priority)),
+                "cuGreenCtxStreamCreate")
     stream = torch.cuda.ExternalStream(int(st), device=torch.device("cuda", device_index))
     return stream, count
 
