@@ -293,7 +293,14 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
     __threadfence();  // this warp's global writes (e.g. the pre-compress own-block max slot) before arriving
     const unsigned prev = atomicAdd(&s_bar_arrived[k], 1u);
     const uint64_t t0 = globaltimer();
-    if (prev == (unsigned)kWarps - 1) {  // last warp of the CTA: the CTA's global arrival
+    if (prev == (unsigned)kWarps - 1 && P.G == 1) {
+      // a one-CTA launch (small calls): the CTA is the whole rank, so the
+      // shared-memory meeting is the barrier -- no global arrival, fence or poll
+      *(volatile float*)&s_bar_vmax[k] = __uint_as_float(*(volatile unsigned*)&s_bar_max[k]);
+      __threadfence_block();
+      *(volatile int*)&s_bar_open[k] = 1;
+      v = *(volatile float*)&s_bar_vmax[k];
+    } else if (prev == (unsigned)kWarps - 1) {  // last warp of the CTA: the CTA's global arrival
       atomicMax(&cb(ctl)->maxslot[k], ((unsigned long long)s_seq << 32) | *(volatile unsigned*)&s_bar_max[k]);
       __threadfence();
       atomicAdd(&cb(ctl)->bar, 1ull);
