@@ -706,7 +706,7 @@ def our_arm(args, ws, rank, local):
         # the smallest real call (16 elements per rank, codec none): calibrates
         # the per-call cost Eq. 5 has no term for (timing.ring_fixed_overhead)
         small = ring_vs_nccl(ep, "none", N, dev, [16 * N])[0]
-        probes = {"S_s": S, "small_call_s": small["none"]["ms"] * 1e-3, "small_n": 16 * N}
+        probes = {"S_s": S, "small_call_s": small["none"]["ms"] * 1e-3, "small_n": 16 * N, "ctas": g}
         if rank == 0:
             probes["gamma_small"] = T.gamma_hop("none", 16, dev, ring_ctas=g)
             for key, m in (("1k", 1024), ("mid", n), ("big", 1 << 26)):
@@ -962,7 +962,8 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
     rows = []
     for row, key in zip(allreduce, ("1k", "mid", "big")):
         rows.append(T.compare_ring(row[codec]["ms"] * 1e-3, N, codec, row["n"], a, b, probes["gamma_" + key], S,
-                                   probes["delta_" + key], fixed_s=fixed))
+                                   probes["delta_" + key], fixed_s=fixed, fence_s=calib.get("phi_s", 0.0),
+                                   fenced_phases=T.ring_fenced_phases(row["n"], N, probes["ctas"], codec)))
     mid = rows[1]
     gam = probes["gamma_mid"]
     cluster = T.ClusterParams(workers=N, latency_s=a, byte_time_s=b, reduce_time_s=gam, sync_time_s=S,
@@ -973,12 +974,14 @@ def timing_model(avg, iso, n, N, w, allreduce, codec, step_ms, calib=None, probe
     rel = (step_ms * 1e-3 - pred_it) / pred_it
     out["eq5"] = {
         "symbols": {"alpha_us": a * 1e6, "beta_push_gbs": calib["push_gbs"],
+                    "phi_fence_us": calib.get("phi_s", 0.0) * 1e6,
                     "gamma_gbs": 1 / gam / 1e9 if gam else None, "S_us": S * 1e6},
         "rings": rows, "step_gradient_ring": mid,
         "note": "measured = the same ring alone, back-to-back, at the engine's CTA budget (the allreduce rows); "
                 "gamma is one fused hop on one GPU on that same budget; eq5_ext adds the step-0 encode, the "
-                "allgather decode and the per-call fixed cost (launch, call open / close: Eq. 5's residual on a "
-                "16-element-per-rank call) the paper's model leaves out (timing.compare_ring)",
+                "allgather decode, the per-call fixed cost (launch, call open / close: Eq. 5's residual on a "
+                "16-element-per-rank call) and the release drain of each flag-protocol phase (phi, measured by "
+                "timing.calibrate_nvlink) the paper's model leaves out (timing.compare_ring)",
         "fixed_per_call_us": fixed * 1e6}
     out["compare_prediction"] = [{"mode": mode, "measured_ms": step_ms, "predicted_ms": pred_it * 1e3,
                                   "rel_error": rel, "flagged": abs(rel) > 0.25,

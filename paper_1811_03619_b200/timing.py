@@ -212,11 +212,66 @@ def calibrate_nvlink(devices=(0, 1), nbytes: int = 1 << 30, ctas: int = 148, ite
     for s in st:
         s.synchronize()
     t = ns[0].item()
-    tr.close()
     if t < 0:  # the kernel's timeout sentinel (~0): the partner never answered
+        tr.close()
         raise RuntimeError("flag ping-pong timed out (is the peer GPU busy with another process?)")
     alpha = t / iters / 2 / 1e9
-    return {"alpha_s": alpha, "beta_s_per_byte": beta, "push_gbs": 1 / beta / 1e9}
+    phi = _fence_tail(devices, a, b, st)
+    tr.close()
+    return {"alpha_s": alpha, "beta_s_per_byte": beta, "push_gbs": 1 / beta / 1e9, "phi_s": phi}
+
+
+def _fence_tail(devices, a, b, st, nbytes: int = 8 << 20, chunk: int = 4096, ctas: int = 148, reps: int = 20) -> float:
+    """phi: what a system-scope release per chunk adds to one phase of
+    pushes (the flag protocol's publish, which Eq. 5's per-hop alpha does not
+    cover): both GPUs push 8 MiB to each other in 4 KiB warp chunks, with and
+    without a st.release.sys flag after every chunk (gp_calib_p2p_copy_ex
+    modes 6 / 2); the difference of the two, per phase."""
+    import torch
+
+    from . import _lib
+
+    ctr = [torch.zeros(reps, dtype=torch.int64, device=f"cuda:{d}") for d in devices]
+    flags = [torch.zeros(nbytes // chunk + 1, dtype=torch.int64, device=f"cuda:{d}") for d in devices]
+    times = {}
+    for mode in (2, 6, 2, 6):
+        for c in ctr:
+            c.zero_()
+        for d in devices:
+            torch.cuda.synchronize(d)
+        ev = []
+        for i, d in enumerate(devices):
+            with torch.cuda.device(d):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st[i])
+                for k in range(reps):
+                    _lib.call("gp_calib_p2p_copy_ex", b[1 - i].data_ptr(), a[i].data_ptr(), nbytes, ctas, mode, chunk,
+                              ctr[i][k:k + 1].data_ptr(), flags[1 - i].data_ptr(), st[i].cuda_stream)
+                e1.record(st[i])
+                ev.append((e0, e1))
+        for s in st:
+            s.synchronize()
+        times[mode] = max(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3 / reps  # the second run of each mode wins
+    return max(0.0, times[6] - times[2])
+
+
+def ring_fenced_phases(n: int, p: int, ctas: int, codec) -> int:
+    """How many phases of a ring call end in system-scope releases (the flag
+    protocol; the LL protocol has none): p - 1 reduce-scatter hops plus the
+    allgather publish, or 2 for codec none's direct reduce-scatter
+    (gp_ring_plan decides, as the launch does)."""
+    import ctypes
+
+    from . import _lib
+    from .compression import as_codec
+
+    if p < 2:
+        return 0
+    out = (ctypes.c_int64 * 5)()
+    _lib.call("gp_ring_plan", int(n), int(p), int(ctas), int(as_codec(codec)), 0, int(n), out)
+    if out[2]:
+        return 0
+    return 2 if out[4] else p
 
 
 def gamma_hop(codec, n: int, device, reps: int = 10, ring_ctas: int = 0) -> float:
@@ -344,7 +399,8 @@ def ring_fixed_overhead(measured_small_s: float, p: int, n_small: int, alpha: fl
 
 
 def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: float, gamma: float, sync: float,
-                 delta: float = 0.0, flag_threshold: float = 0.25, fixed_s: float = 0.0) -> dict:
+                 delta: float = 0.0, flag_threshold: float = 0.25, fixed_s: float = 0.0, fence_s: float = 0.0,
+                 fenced_phases: int = 0) -> dict:
     """One prediction-vs-measurement row for a ring call (compare_prediction,
     harness.py:687-720, applied to Eq. 5 itself): n is the element count,
     model bytes are the codec's payload (harness.py:562).
@@ -356,7 +412,9 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
     (p-1)/p n delta (delta = decode time per element). For none / trunc16 the
     step-0 encode streams straight onto the link and the decode overlaps the
     owners' pushes. Every codec's eq5_ext also adds `fixed_s`, the per-call
-    cost calibrated on the smallest call (ring_fixed_overhead)."""
+    cost calibrated on the smallest call (ring_fixed_overhead), and, for the
+    flag protocol, `fenced_phases` x `fence_s` (ring_fenced_phases; phi from
+    calibrate_nvlink): the release drain that ends each phase."""
     from .compression import as_codec
 
     nb = float(n * as_codec(codec).bytes_per_elem)
@@ -367,13 +425,14 @@ def compare_ring(measured_s: float, p: int, codec, n: int, alpha: float, beta: f
     q8 = as_codec(codec).name.lower() == "quant8"
     step0 = nb / p * gamma if (p > 1 and q8) else 0.0
     ag = (p - 1) / p * n * delta if q8 else 0.0
-    ext = pred + step0 + ag + fixed_s
+    fence = fenced_phases * fence_s
+    ext = pred + step0 + ag + fixed_s + fence
     rel = (measured_s - pred) / pred if pred > 0 else float("inf")
     rel_ext = (measured_s - ext) / ext if ext > 0 else float("inf")
     return {"n": n, "codec": as_codec(codec).name.lower(), "measured_ms": measured_s * 1e3, "eq5_ms": pred * 1e3,
             "terms_us": {"latency": lat * 1e6, "bandwidth": bw * 1e6, "reduction": red * 1e6, "sync": syn * 1e6,
                          "ext_step0_encode": step0 * 1e6, "ext_allgather_decode": ag * 1e6,
-                         "ext_fixed_per_call": fixed_s * 1e6},
+                         "ext_fixed_per_call": fixed_s * 1e6, "ext_fence_drain": fence * 1e6},
             "eq5_over_measured": pred / measured_s if measured_s > 0 else None, "rel_error": rel,
             "flagged": abs(rel) > flag_threshold,
             "eq5_ext_ms": ext * 1e3, "eq5_ext_over_measured": ext / measured_s if measured_s > 0 else None,

@@ -123,3 +123,22 @@ def test_ring_fixed_overhead_is_eq5_residual_on_the_smallest_call():
     assert row["eq5_ms"] == row0["eq5_ms"]
     assert row["eq5_ext_ms"] == pytest.approx(row0["eq5_ext_ms"] + 7e-3, rel=1e-9)
     assert row["terms_us"]["ext_fixed_per_call"] == pytest.approx(7.0)
+
+
+def test_fenced_phases_follow_the_launch_plan():
+    """timing.ring_fenced_phases: LL calls publish without releases; the flag
+    protocol ends p phases in a release (p - 1 hops + the allgather), codec
+    none's direct reduce-scatter 2; compare_ring adds phases x phi to eq5_ext
+    only."""
+    from paper_1811_03619_b200 import timing as T
+    assert T.ring_fenced_phases(4099, 4, 592, "none") == 0           # LL
+    assert T.ring_fenced_phases(16_777_216, 2, 592, "none") == 2     # flag, ring
+    assert T.ring_fenced_phases(16_777_216, 4, 592, "trunc16") == 4  # flag, ring
+    assert T.ring_fenced_phases(16_777_216, 4, 592, "none") == 2     # flag, direct reduce-scatter
+    assert T.ring_fenced_phases(100, 1, 592, "none") == 0
+    a, b, g, S = 2e-6, 1 / 700e9, 1 / 400e9, 5e-6
+    r0 = T.compare_ring(1e-4, 4, "trunc16", 16_777_216, a, b, g, S)
+    r1 = T.compare_ring(1e-4, 4, "trunc16", 16_777_216, a, b, g, S, fence_s=6e-6, fenced_phases=4)
+    assert r1["eq5_ms"] == r0["eq5_ms"]
+    assert r1["eq5_ext_ms"] == pytest.approx(r0["eq5_ext_ms"] + 0.024, rel=1e-9)
+    assert r1["terms_us"]["ext_fence_drain"] == pytest.approx(24.0)

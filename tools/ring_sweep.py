@@ -182,7 +182,8 @@ def main():
                 gam = T.gamma_hop(codec, max(1, n // p), dv, ring_ctas=ep.info()["ctas"])
                 dlt = T.delta_decode(codec, max(1, n // p), dv)
                 rec["eq5"] = T.compare_ring(t, p, codec, n, sym["alpha_s"], sym["beta_s_per_byte"], gam, sym["S_s"],
-                                            dlt, fixed_s=sym.get("fixed_s", 0.0))
+                                            dlt, fixed_s=sym.get("fixed_s", 0.0), fence_s=sym.get("phi_s", 0.0),
+                                            fenced_phases=T.ring_fenced_phases(n, p, ep.info()["ctas"], codec))
                 rec["eq5"]["gamma_gbs"] = 1 / gam / 1e9 if gam > 0 else None
             if args.cpu_ref_max and n <= args.cpu_ref_max:
                 dist.barrier()
