@@ -360,6 +360,9 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
 #ifndef PIPESGD_Q8_UNROLL
 #define PIPESGD_Q8_UNROLL 1
 #endif
+#ifndef PIPESGD_LL_STATIC
+#define PIPESGD_LL_STATIC 1
+#endif
 #ifndef PIPESGD_LL_UNROLL
 #define PIPESGD_LL_UNROLL 1
 #endif
@@ -502,6 +505,15 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   float* out = R.out;
   const bool slot_mode = R.slot != nullptr;
   int bad = 0;
+  // Next chunk of a phase for this warp. The flag protocol takes it from the
+  // phase counter (fast warps take more chunks: NVLink arbitration gives
+  // warps unequal shares); the LL protocol strides statically -- its chunks
+  // are short, so a shared counter meant thousands of same-address atomics
+  // per phase on large LL blocks, and its warps wait on the data anyway.
+  auto next = [&](int phase, uint32_t cur) -> uint32_t {
+    if constexpr (LL && PIPESGD_LL_STATIC) return cur + NW;
+    else return grab(ctl, phase, NW);
+  };
   stamp(P, wid, lr, 0);
 #ifdef PIPESGD_CHECKED
   if (P.selftest && wid == 0 && out != nullptr) {  // negative control: one group past the end of out
@@ -608,7 +620,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     for (int b = 0; b < p; ++b) NCH = max(NCH, get_blk(P, b).nch);
     const Q8 q = q8_make(0.f);
     // send: block b = (r - d) % p goes to its owner (b - 1) % p, slot d
-    for (uint32_t j = wid; j < (uint32_t)(p - 1) * NCH; j = grab(ctl, 1, NW)) {
+    for (uint32_t j = wid; j < (uint32_t)(p - 1) * NCH; j = next(1, j)) {
       const int d = (int)(j / NCH);
       const uint32_t c = j % NCH;
       const int b = (r - d + p) % p;
@@ -635,7 +647,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const Blk B = get_blk(P, own);
     constexpr int U = LL ? 1 : 2;  // groups per lane per batch: U x p loads in flight
     bool first = true;
-    for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2, NW)) {
+    for (uint32_t c = wid; c < B.nch; c = next(2, c)) {
       if (ll) {
         float sdum;
         for (int d = 0; d < p - 1; ++d)
@@ -727,7 +739,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         if constexpr (!PRE) {
           uint32_t m = 0;
           const uint64_t keep = l2_evict_last();  // the send pass below re-reads the block
-          for (uint32_t c = wid; c < B.nch; c = grab(ctl, 0, NW))
+          for (uint32_t c = wid; c < B.nch; c = next(0, c))
             for_groups<C, LL>(P, B, c,
                           [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) {
                             return load_fv_pol<E>(x, g0, lo, hi, keep);
@@ -743,7 +755,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
           W.start = 0; W.len = P.n; W.A = 0;
           W.nch = P.n ? (uint32_t)((P.n + P.chunk - 1) / P.chunk) : 0u;
           uint32_t m = 0, mo = 0;
-          for (uint32_t c = wid; c < W.nch; c = grab(ctl, 0, NW))
+          for (uint32_t c = wid; c < W.nch; c = next(0, c))
             for_groups<C, LL>(P, W, c,
                           [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                           [&](uint64_t g0, uint64_t, uint64_t, int, int, const FV<E>& v) {
@@ -771,7 +783,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       uint8_t* dst = slot_ptr(R.peer[succ], P.L, rs_slot(0));
       uint8_t* lld = ll_ptr(R.peer[succ], P.L, rs_slot(0));
       bool first0 = true;
-      for (uint32_t c = wid; c < B.nch; c = grab(ctl, 1, NW)) {
+      for (uint32_t c = wid; c < B.nch; c = next(1, c)) {
         for_groups<C, LL>(P, B, c,
                       [&](uint64_t g0, uint64_t lo, uint64_t hi, int, int) { return load_fv<E>(x, g0, lo, hi); },
                       [&](uint64_t g0, uint64_t, uint64_t, int vlo, int vhi, const FV<E>& v) {
@@ -837,7 +849,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
       if constexpr (C != kQuant8) {
         const Q8 q = q8_make(0.f);
         bool first = true;
-        for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2 + 2 * s, NW)) {
+        for (uint32_t c = wid; c < B.nch; c = next(2 + 2 * s, c)) {
           float sin = 0.f;
           stamp2(P, wid, lr, 4, first);
           if (ll) {
@@ -876,7 +888,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         };
         uint32_t m = 0;
         bool first = true;
-        for (uint32_t c = wid; c < B.nch; c = grab(ctl, 2 + 2 * s, NW)) {
+        for (uint32_t c = wid; c < B.nch; c = next(2 + 2 * s, c)) {
           float sin;
           if (ll) {
             if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
@@ -904,7 +916,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
         // push it. Any warp may take any chunk: the chunk's flag (or LL
         // lines) already carries this call's sequence, so the waits below
         // return at once and hand this warp the chunk's incoming scale.
-        for (uint32_t c = wid; c < B.nch; c = grab(ctl, 3 + 2 * s, NW)) {
+        for (uint32_t c = wid; c < B.nch; c = next(3 + 2 * s, c)) {
           float sin;
           if (ll) {
             if (!ll_hdr_get(ll_in, c, kPhRS, s, b, B.len, sin)) return;
@@ -980,7 +992,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const uint8_t* in_slot = slot_ptr(R.inbox, P.L, ag_slot(p, b));
     const uint8_t* ll_in = ll_ptr(R.inbox, P.L, ag_slot(p, b));
     bool first = true;
-    for (uint32_t c = wid; c < B.nch; c = grab(ctl, 20 + k, NW)) {
+    for (uint32_t c = wid; c < B.nch; c = next(20 + k, c)) {
       float sin = 0.f;
       stamp2(P, wid, lr, 9, first && k == 1);
       if (ll) {
