@@ -34,6 +34,11 @@ for codec in (0, 1, 2):
         want = OE.run_trajectory(p, OE.Config(mode=mode, iterations=7, learning_rate=0.1, codec=codec,
                                               batch_size=16, seed=7), data, net).params
         out[f"{mode}_{codec}"] = bool(res.params.tobytes() == want.tobytes())
+        if mode == "pipe_sgd":  # the comm stream in a 16-SM green context (engine.default_comm_partition's path)
+            rng = np.random.default_rng([7, rank])
+            res = run_process_worker(cfg, data, ModelSpec("mlp", (8, 16, 12, 3)), grad_fn=grad_fn, comm_sms=16,
+                                     comm_ctas=64)
+            out[f"{mode}_{codec}_partition"] = bool(res.params.tobytes() == want.tobytes())
 if rank == 0:
     print(json.dumps(out))
 dist.barrier()
