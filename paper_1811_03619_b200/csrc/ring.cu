@@ -192,7 +192,7 @@ __device__ uint64_t spin_flag(const uint64_t* f, const RingParams& P, const Rank
     if (ns < 256) ns <<= 1;
     if ((it & 63u) == 0) {
       if (aborted(P, ctl)) {
-        latch_error(err, kErrTimeout, phase, step, block, R.rank, abort_detail(ctl, R.rank));
+        latch_error(err, kErrTimeout, phase, step, block, R.rank, kAbortConsequence);
         return 0;
       }
       if (globaltimer() - t0 > P.timeout_ns) {
@@ -309,7 +309,7 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
         __nanosleep(32);
         if ((it & 63u) == 0) {
           if (aborted(P, ctl)) {
-            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, abort_detail(ctl, R.rank));
+            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, kAbortConsequence);
             ok = 0;
             break;
           }
@@ -332,7 +332,7 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
         __nanosleep(32);
         if ((it & 63u) == 0) {
           if (aborted(P, ctl)) {
-            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, abort_detail(ctl, R.rank));
+            latch_error(err, kErrTimeout, kPhBarrier, step, -1, R.rank, kAbortConsequence);
             st = 2;
             break;
           }
@@ -359,6 +359,16 @@ __device__ bool warp_barrier_max(const RingParams& P, const RankCtx& R, Ctl* ctl
 // all loads of a batch are issued before any of its stores.
 #ifndef PIPESGD_Q8_UNROLL
 #define PIPESGD_Q8_UNROLL 1
+#endif
+#ifndef PIPESGD_FLAG_STATIC
+#define PIPESGD_FLAG_STATIC 0  // A/B knob: static chunk stride for the flag protocol too
+#endif
+// Direct reduce-scatter send jobs destination-fastest (job j -> peer j % (p-1),
+// chunk j / (p-1)), so every moment's stores spread over all owners: p = 4
+// codec none 64 MiB 202 -> 195 us, 256 MiB 686-724 -> 675 us
+// (profiles/r02/direct_order_ab/); 0 = block-major.
+#ifndef PIPESGD_DIRECT_INTERLEAVE
+#define PIPESGD_DIRECT_INTERLEAVE 1
 #endif
 #ifndef PIPESGD_LL_STATIC
 #define PIPESGD_LL_STATIC 1
@@ -511,7 +521,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   // are short, so a shared counter meant thousands of same-address atomics
   // per phase on large LL blocks, and its warps wait on the data anyway.
   auto next = [&](int phase, uint32_t cur) -> uint32_t {
-    if constexpr (LL && PIPESGD_LL_STATIC) return cur + NW;
+    if constexpr ((LL && PIPESGD_LL_STATIC) || PIPESGD_FLAG_STATIC) return cur + NW;
     else return grab(ctl, phase, NW);
   };
   stamp(P, wid, lr, 0);
@@ -558,7 +568,7 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   auto give_up = [&]() -> bool {
     if (ll_fail) return true;
     if (aborted(P, ctl)) {
-      ll_fail = abort_detail(ctl, r) == 0 ? 3 : 2;  // 3: this rank's own abort (same missing peer)
+      ll_fail = 2;  // an abort (this rank's or a peer's): a consequence
       return true;
     }
     const uint64_t now = globaltimer();
@@ -578,11 +588,10 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
   };
   // warp: any lane gave up -> latch like warp_await and leave
   auto ll_ok = [&](int phase, int step, int block) -> bool {
-    const int any = __any_sync(0xffffffffu, ll_fail != 0), own = __any_sync(0xffffffffu, ll_fail == 1),
-              mine = __any_sync(0xffffffffu, ll_fail == 3);
+    const int any = __any_sync(0xffffffffu, ll_fail != 0), own = __any_sync(0xffffffffu, ll_fail == 1);
     if (!any) return true;
     if (lane_id() == 0) {
-      latch_error(err, kErrTimeout, phase, step, block, r, (own || mine) ? 0 : 1);
+      latch_error(err, kErrTimeout, phase, step, block, r, own ? 0 : kAbortConsequence);
       if (own) broadcast_abort(P, R);
     }
     return false;
@@ -621,8 +630,8 @@ __device__ __forceinline__ void ring_body(const RingParams& P) {
     const Q8 q = q8_make(0.f);
     // send: block b = (r - d) % p goes to its owner (b - 1) % p, slot d
     for (uint32_t j = wid; j < (uint32_t)(p - 1) * NCH; j = next(1, j)) {
-      const int d = (int)(j / NCH);
-      const uint32_t c = j % NCH;
+      const int d = PIPESGD_DIRECT_INTERLEAVE ? (int)(j % (uint32_t)(p - 1)) : (int)(j / NCH);
+      const uint32_t c = PIPESGD_DIRECT_INTERLEAVE ? j / (uint32_t)(p - 1) : j % NCH;
       const int b = (r - d + p) % p;
       const Blk B = get_blk(P, b);
       if (c >= B.nch) continue;

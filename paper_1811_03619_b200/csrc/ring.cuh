@@ -91,11 +91,13 @@ __device__ __forceinline__ unsigned long long abort_word(const Ctl* ctl) {
   return *(const volatile unsigned long long*)&ctl->abort;
 }
 __device__ __forceinline__ bool comm_aborted(const Ctl* ctl) { return (abort_word(ctl) & kAbortSticky) != 0; }
-// detail of the error a warp latches when it stops on an abort: 0 = this
-// rank's own timeout (another warp of the rank gave up first), 1 = a peer failed
-__device__ __forceinline__ int abort_detail(const Ctl* ctl, int rank) {
-  return (int)((abort_word(ctl) >> 32) & 0xFF) == rank + 1 ? 0 : 1;
-}
+// A warp that stops on an abort latches a consequence (timeout kind, detail
+// 1), whichever rank raised it: the warp that raised it has latched the cause
+// itself (its own timeout, a header mismatch, ...) before broadcasting, and a
+// cause outranks every consequence in the error word. (Reporting this rank's
+// own abort as another timeout let it outrank a header mismatch at the same
+// step, since timeout sorts first.)
+constexpr int kAbortConsequence = 1;
 
 // Poison this communicator on every rank (peers' ctl blocks over NVLink).
 // Out of line: an error path, reached from every wait site.

@@ -71,7 +71,7 @@ __device__ bool star_wait(const uint64_t* f, const StarParams& P, const StarRank
     if (ns < 512) ns <<= 1;
     if ((it & 31u) == 0) {
       if (comm_aborted(ctl)) {
-        latch_error(err, kErrTimeout, phase, 0, src, rank, abort_detail(ctl, rank));
+        latch_error(err, kErrTimeout, phase, 0, src, rank, kAbortConsequence);
         return false;
       }
       if (globaltimer() - t0 > P.timeout_ns) {
