@@ -4,8 +4,8 @@ cd "$(dirname "$0")/.."
 O=gpurun_out/${TAG:-r02_green2}
 mkdir -p $O
 run() {  # model sms ctas steps
-  BENCH_COMM_SMS=$2 timeout 420 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
-    --master-port 29731 bench.py --gpus 4 --model $1 --ctas $3 --no-allreduce-sweep --steps $4 \
+  timeout 420 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+    --master-port 29731 bench.py --gpus 4 --model $1 --comm-sms $2 --ctas $3 --no-allreduce-sweep --steps $4 \
     > $O/$1_sms$2_c$3.json 2> $O/$1_sms$2_c$3.err
 }
 run c3 24 96 20
