@@ -114,6 +114,23 @@ def test_c3_c4_on_real_gpus(P, codec, n):
     check_blocks(base, outs, codec)
 
 
+@pytest.mark.parametrize("codec", [1, 2])
+@pytest.mark.parametrize("scale", [1e-38, 1e-6, 1e6, 1e30])
+def test_scaled_inputs_on_real_gpus(P, codec, scale):
+    """SURVEY 8(d)'s second input variant: N(0,1) x 10^k, here down to where
+    quant8 block scales are subnormal (1e-38) and up to 1e30; per-rank
+    launches, a non-divisible n, every block bit-exact with the oracle."""
+    p, n = 4, 4_194_307
+    base = make_inputs(p, n, scale, 11)
+    tr = real_transport(P, p, timeout_s=60.0, max_elems=n)
+    ins = [x.to(tr.endpoint(r).device) for r, x in enumerate(base)]
+    try:
+        outs = run_ranks(tr, lambda r, ep: P.ring_allreduce(ins[r], r, p, ep, P.Codec(codec), iteration=5))
+    finally:
+        tr.close()
+    check_blocks(base, outs, codec)
+
+
 def test_c1_mnist_mlp_pipe_sgd_bit_exact(P):
     """C1: MLP 784-500-500-10, p=4, codec none, width 2, global batch 100."""
     from paper_1811_03619_b200.engine import RunConfig, run_inproc_cluster
