@@ -222,7 +222,8 @@ class RankEngine:
         self.ms = torch.cuda.Stream(self.dev, priority=prio)
         # comm_sms > 0: the comm stream lives in a green context of that many
         # SMs (greenctx.py), so the pipelined ring occupies a fixed slice of
-        # the GPU; the communicator's CTA budget must fit it (4 CTAs per SM)
+        # the GPU; the communicator's CTA budget must fit it (4 CTAs per SM;
+        # ranks sharing a GPU share the slice, so their budgets together)
         self.comm_sms = 0
         if comm_sms > 0:
             from .greenctx import green_stream

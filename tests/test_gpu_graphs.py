@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0):
+def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0, comm_sms=0):
     from paper_1811_03619_b200.engine import RankEngine, RunConfig
     from paper_1811_03619_b200.models import FlatModel, ModelSpec, SpecNet, init_params
     spec = ModelSpec("mlp", (64, 128, 10))
@@ -29,7 +29,7 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0):
             y = torch.randint(0, 10, (32,), generator=g).to(dev)
             cfg = RunConfig(mode=mode, iterations=T + 2, learning_rate=0.05, codec=codec, batch_size=32, depth=depth,
                             lr_decay_every=decay, lr_decay_factor=0.5 if decay else 1.0)
-            eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False)
+            eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False, comm_sms=comm_sms)
             pipe = mode == "pipe_sgd"
             step = eng.step if pipe else eng.step_sync
             with torch.cuda.stream(eng.cs):
@@ -93,3 +93,16 @@ def test_graph_replay_with_lr_decay_matches_eager(P, p, mode):
         np.testing.assert_array_equal(graph[r][1], eager[r][1])
     const = train(P, p, 1, graphs=True, mode=mode, decay=0)
     assert not np.array_equal(const[0][0], graph[0][0]), "decay had no effect"
+
+
+@pytest.mark.parametrize("codec", [0, 2])
+def test_graph_replay_on_green_context_stream_matches_eager(P, codec):
+    """The bench's configuration at N > 1: comm graphs captured and replayed
+    on a green-context stream (RankEngine comm_sms) give the eager engine's
+    weights bit for bit."""
+    eager = train(P, 2, codec, graphs=False)
+    # 32 SMs x 4 CTAs hold both ranks' 64-CTA rings when they share one GPU
+    graph = train(P, 2, codec, graphs=True, comm_sms=32)
+    for r in range(2):
+        assert_bits_equal(graph[r][0], eager[r][0], f"green graphs codec={codec} rank {r}")
+        np.testing.assert_array_equal(graph[r][1], eager[r][1])
