@@ -154,3 +154,12 @@ def test_default_comm_partition_policy():
     assert default_comm_ctas("pipe_sgd", 61_100_840) == 256
     assert default_comm_ctas("pipe_sgd", 648_010) == 64
     assert default_comm_ctas("pipe_sgd", 4_700_000) == 64
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_green_stream_fails_cleanly_without_a_gpu():
+    """greenctx.green_stream raises (RankEngine then warns and keeps a plain
+    comm stream) instead of crashing when there is no driver or device."""
+    from paper_1811_03619_b200.greenctx import green_stream
+    with pytest.raises(Exception):
+        green_stream(0, 16)
