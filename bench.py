@@ -63,7 +63,7 @@ def parse():
                          "0: no partition)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--graphs", type=int, default=1,
-                    help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync, fused)")
+                    help="replay the steady-state step as CUDA graphs (pipe_sgd / d_sync / ps_sync, fused)")
     ap.add_argument("--fused", type=int, default=1,
                     help="one comm kernel per step (pre-compress + ring + re-compress fused)")
     ap.add_argument("--channels-last", type=int, default=0,
@@ -380,7 +380,7 @@ def workload_config(args, n, N):
             "model": model, "params": n, "global_batch": args.global_batch,
             "per_gpu_batch": args.global_batch // max(N, 1), "codec": args.codec,
             "mode": args.mode, "depth": width, "parallelism": f"dp{N}",
-            "cuda_graphs": bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused),
+            "cuda_graphs": bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync", "ps_sync") and bool(args.fused),
             "ring_ctas": args.ctas if args.ctas > 0 else None,
             "comm_partition_sms": args.comm_sms or None,
             "model_math": "fp32 (TF32 disabled for cuDNN convolutions and cuBLAS matmuls)",
@@ -430,7 +430,7 @@ def our_arm(args, ws, rank, local):
         x_host = x_host.contiguous(memory_format=torch.channels_last).pin_memory()
     x_dev, y_dev = x_host.to(dev), y_host.to(dev)
     mode = {"e2e": False, "end": 0}
-    use_graphs = bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync") and bool(args.fused)
+    use_graphs = bool(args.graphs) and args.mode in ("pipe_sgd", "d_sync", "ps_sync") and bool(args.fused)
     # Inputs: one buffer per pipeline parity. In e2e mode step t's batch is
     # copied from pinned host memory into buffer t % NB on a copy stream while
     # step t-1 computes (every step's copy stays inside the timed region);

@@ -472,8 +472,8 @@ class RankEngine:
         static batch tensors (refilled in place by the caller). Learning-rate
         decay works: the update graphs read the rate from device memory."""
         cfg = self.cfg
-        if not self.fused or cfg.mode not in (MODE_PIPE_SGD, MODE_D_SYNC) or self.grad_fn is not None:
-            raise ConfigError("graph mode needs fused pipe_sgd or d_sync and a model")
+        if not self.fused or cfg.mode not in (MODE_PIPE_SGD, MODE_D_SYNC, MODE_PS_SYNC) or self.grad_fn is not None:
+            raise ConfigError("graph mode needs fused pipe_sgd, d_sync or ps_sync and a model")
         if cfg.eval_interval or cfg.snapshot_first:
             # their host-side snapshots live in the eager step (engine.py run()
             # keeps them); a replayed step would silently skip them
@@ -506,6 +506,8 @@ class RankEngine:
         try:
             if cfg.mode == MODE_D_SYNC:
                 self._capture_sync_graphs(batches, lr)
+            elif cfg.mode == MODE_PS_SYNC:
+                self._capture_ps_graphs(batches, lr)
             else:
                 self._capture_pipe_graphs(batches, lr)
         finally:
@@ -561,6 +563,55 @@ class RankEngine:
             self.g_comm.append(gm)
         self.graph_pending = None
 
+    def _capture_ps_graphs(self, batches, lr) -> None:
+        """ps_sync as graphs, parity i = t % K: compute (forward/backward into
+        gradient buffer i, zeroing it first like the eager step), compress
+        (local D(C(grad))) and the star round (gather to the root, the root's
+        SGD step with the device-resident rate, broadcast of the parameters)
+        -- ps_step's kernels in ps_step's order. The star kernels read their
+        call sequence on the device, so every replay is a new call; the
+        iteration tag they carry is the capture step's, the same on every rank."""
+        K, codec, root = self.K, self.cfg.codec, 0
+        for i in range(K):
+            gc = torch.cuda.CUDAGraph()
+            with capture(gc, self.cs):
+                self.fm.use_grad_buffer(i)
+                self.static_loss[i].copy_(self.fm.loss_and_grad(*batches[i]))
+            gz = torch.cuda.CUDAGraph()
+            with capture(gz, self.cs):
+                roundtrip_async(self.fm.grad_bufs[i], codec, self.local[i], self.local_status[i], self.cs.cuda_stream)
+            gm = torch.cuda.CUDAGraph()
+            with capture(gm, self.cs):
+                self.ep._star(self.local[i], self.summed if self.rank == root else None, self.n, root, 0, True, 0,
+                              self.cs)
+                if self.rank == root:
+                    _lib.call("gp_consume_update_dev", self.fm.params.data_ptr(), int(Codec.NONE),
+                              self.summed.data_ptr(), self.local_status[i].scale_view.data_ptr(), self.n,
+                              lr.data_ptr(), self.world, self.cs.cuda_stream)
+                self.ep._star(self.fm.params, self.fm.params, self.n, root, 1, False, 0, self.cs)
+            self.g_compute.append(gc)
+            self.g_update.append(gz)  # the compress graph
+            self.g_comm.append(gm)
+
+    def _step_graph_ps(self, t: int) -> None:
+        i = t % self.K
+        tr = self.tracing
+        self._set_lr(t)
+        e0 = self._ev(self.cs) if tr else None
+        self.g_compute[i].replay()
+        self.losses[t].copy_(self.static_loss[i])
+        e1 = self._ev(self.cs) if tr else None
+        self.g_update[i].replay()
+        e2 = self._ev(self.cs) if tr else None
+        self.g_comm[i].replay()
+        if tr:
+            e3 = self._ev(self.cs)
+            self._rec(t, STAGE_BACKWARD, e0, e1)
+            self._rec(t, STAGE_COMPRESS, e1, e2)
+            self._rec(t, STAGE_ALLREDUCE, e2, e3)
+        self.updates_seen += 1
+        self._mark(t)
+
     def _step_graph_sync(self, t: int) -> None:
         """d_sync by replay: the graph consumes t-1 itself, so only an eager
         predecessor (the warm-up's last step) has to be waited for."""
@@ -597,6 +648,9 @@ class RankEngine:
         """One iteration by graph replay (after prime / eager warm-up)."""
         if self.cfg.mode == MODE_D_SYNC:
             self._step_graph_sync(t)
+            return
+        if self.cfg.mode == MODE_PS_SYNC:
+            self._step_graph_ps(t)
             return
         i = t % self.K
         prev = self.graph_ready_tag.pop(i, None)
@@ -638,6 +692,8 @@ class RankEngine:
 
     def drain_graph(self, t1: int) -> None:
         """The last updates eagerly, with the eager engine's rates (drain / drain_sync)."""
+        if self.cfg.mode == MODE_PS_SYNC:
+            return  # every step applied its own update
         if self.cfg.mode == MODE_D_SYNC:
             if self.graph_pending is not None:
                 pend = self.sync_slots[self.graph_pending % self.K]

@@ -31,7 +31,7 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0, com
                             lr_decay_every=decay, lr_decay_factor=0.5 if decay else 1.0)
             eng = RankEngine(r, p, ep, fm, cfg, lambda rank, t: (x, y), trace=False, comm_sms=comm_sms)
             pipe = mode == "pipe_sgd"
-            step = eng.step if pipe else eng.step_sync
+            step = eng.step if pipe else eng.ps_step if mode == "ps_sync" else eng.step_sync
             with torch.cuda.stream(eng.cs):
                 if pipe:
                     eng.prime(1)
@@ -45,7 +45,10 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0, com
                 else:
                     for t in range(W + 1, T + 1):
                         step(t)
-                    eng.drain(T) if pipe else eng.drain_sync()
+                    if pipe:
+                        eng.drain(T)
+                    elif mode == "d_sync":
+                        eng.drain_sync()
             eng.cs.synchronize()
             eng.ms.synchronize()
             ep._check_errors(fm.num_params)
@@ -57,7 +60,7 @@ def train(P, p, codec, graphs, T=12, W=3, mode="pipe_sgd", depth=2, decay=0, com
         tr.close()
 
 
-@pytest.mark.parametrize("mode", ["pipe_sgd", "d_sync"])
+@pytest.mark.parametrize("mode", ["pipe_sgd", "d_sync", "ps_sync"])
 @pytest.mark.parametrize("codec", [0, 1, 2])
 @pytest.mark.parametrize("p", [1, 2])
 def test_graph_replay_matches_eager(P, p, codec, mode):
